@@ -1,0 +1,178 @@
+"""Pins for the oracle's thresholds, rules and ITA loop (oracle/ita.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import configs, synth
+from inputs.configs import SarParams
+from oracle import csa, echo, ita
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand(shape, seed, scale=1.0):
+    r = np.random.default_rng(seed)
+    return scale * (r.standard_normal(shape) + 1j * r.standard_normal(shape))
+
+
+# ---------------------------------------------------------------- thresholds
+def test_soft_worked_example_and_identity():
+    g = json.load(open(os.path.join(GOLD, "spec_worked_examples.json")))
+    out = ita.soft(np.array([3 + 4j]), 2.0)[0]
+    assert abs(out - complex(*g["soft_3p4j_sigma2"])) < 1e-15
+    b = _rand(100, 1)
+    assert np.array_equal(ita.soft(b, 0.0), b)
+    assert not np.any(ita.soft(b, np.abs(b).max()))      # strict survival: full kill
+
+
+def test_soft_nonexpansive():
+    """||E(x) - E(z)|| <= ||x - z||."""
+    for s in range(20):
+        x, z = _rand(200, 2 * s), _rand(200, 2 * s + 1)
+        sig = 0.3 + 0.1 * s
+        assert np.linalg.norm(ita.soft(x, sig) - ita.soft(z, sig)) <= np.linalg.norm(x - z) + 1e-15
+
+
+def _brute_half(a, lm):
+    """argmin_{t >= 0} (t - a)^2 + lm sqrt(t): dense grid then golden-section refinement."""
+    f = lambda t: (t - a) ** 2 + lm * np.sqrt(max(t, 0.0))
+    ts = np.linspace(0.0, a, 20001)
+    vals = (ts - a) ** 2 + lm * np.sqrt(ts)
+    i = int(np.argmin(vals))
+    lo, hi = ts[max(i - 1, 0)], ts[min(i + 1, ts.size - 1)]
+    gr = (np.sqrt(5) - 1) / 2
+    for _ in range(200):
+        c, d = hi - gr * (hi - lo), lo + gr * (hi - lo)
+        if f(c) < f(d):
+            hi = d
+        else:
+            lo = c
+    t = 0.5 * (lo + hi)
+    if t > 0:
+        # polish: bisection on f'(t) = 2(t - a) + lm / (2 sqrt t), increasing near the minimiser
+        df = lambda u: 2.0 * (u - a) + lm / (2.0 * np.sqrt(u))
+        lo, hi = max(t - 1e-3 * a, 1e-300), min(t + 1e-3 * a, a)
+        if df(lo) < 0 < df(hi):
+            for _ in range(200):
+                mid = 0.5 * (lo + hi)
+                if df(mid) < 0:
+                    lo = mid
+                else:
+                    hi = mid
+            t = 0.5 * (lo + hi)
+    return 0.0 if f(0.0) <= f(t) else t
+
+
+def test_half_matches_bruteforce_minimiser():
+    """R15: the q=1/2 operator is the exact minimiser of (t - |b|)^2 + lambda mu sqrt(t)."""
+    r = np.random.default_rng(5)
+    for _ in range(150):
+        sigma = r.uniform(0.1, 3.0)
+        lm = ita.HALF_LM_PER_SIGMA32 * sigma ** 1.5
+        assert ita.half_sigma_from_lm(lm) == pytest.approx(sigma, rel=1e-12)
+        a = r.uniform(0.0, 3.0 * sigma)
+        if abs(a - sigma) < 1e-3 * sigma:
+            continue                      # at the jump both minima tie
+        ph = np.exp(1j * r.uniform(0, 2 * np.pi))
+        h = ita.half(np.array([a * ph]), sigma)[0]
+        t = _brute_half(a, lm)
+        assert abs(abs(h) - t) <= 1e-9 * max(1.0, a)
+        if t > 0:
+            assert abs(np.angle(h / ph)) < 1e-12
+
+
+def test_half_jump_and_identity():
+    s = 1.7
+    just = ita.half(np.array([s * (1 + 1e-12)]), s)[0]
+    assert abs(just - 2 * s / 3) < 1e-9
+    assert ita.half(np.array([s]), s)[0] == 0
+    b = _rand(50, 3)
+    assert np.array_equal(ita.half(b, 0.0), b)
+    g = json.load(open(os.path.join(GOLD, "survey_8c7_anchors.json")))
+    assert abs(ita.half(np.array([3 + 4j]), 2.0)[0] - complex(*g["thresholds_3p4j_sigma2"]["half"])) < 1e-11
+
+
+# ---------------------------------------------------------------- rules
+def test_k_rule_worked_examples():
+    """SPEC S:L365-366 restating P:L316-320."""
+    g = json.load(open(os.path.join(GOLD, "spec_worked_examples.json")))
+    b = np.array(g["k_rule_mags"], dtype=complex) * np.exp(1j * np.arange(5))
+    sig = ita.sigma_k_rule(b, g["k_rule_k"])
+    assert sig == pytest.approx(g["k_rule_sigma"], rel=1e-14)
+    assert np.count_nonzero(ita.soft(b, sig)) == g["k_rule_survivors"]
+    eq = np.full(7, 2.0 + 0j)
+    assert np.count_nonzero(ita.soft(eq, ita.sigma_k_rule(eq, 3))) == 0     # ties killed
+    bb = _rand(30, 9)
+    assert ita.sigma_k_rule(bb, 29) == pytest.approx(np.abs(bb).min())      # k = n - 1 boundary
+    with pytest.raises(ValueError):
+        ita.sigma_k_rule(bb, 30)
+    with pytest.raises(ValueError):
+        ita.sigma_k_rule(bb, 0)
+
+
+# ---------------------------------------------------------------- ITA loop
+def test_ita_full_sampling_one_step_fixed_point():
+    """Theta = 1 and G unitary: every iterate equals E(M Y; sigma(M Y)) (closed form)."""
+    p = SarParams(n_az=64, n_rg=64)
+    op = csa.CSAOperator(p)
+    Y = _rand(op.shape, 11)
+    m = np.ones(op.shape)
+    k = 40
+    b = op.M(Y)
+    ref = ita.soft(b, ita.sigma_k_rule(b, k))
+    for it in (1, 2, 5):
+        X = ita.ita(op, Y, m, thr="soft", rule="k", k=k, iters=it)
+        assert np.max(np.abs(X - ref)) <= 1e-12 * np.max(np.abs(ref))
+    Xh = ita.ita(op, Y, m, thr="half", rule="k", k=k, iters=3)
+    refh = ita.half(b, ita.sigma_k_rule(b, k))
+    assert np.max(np.abs(Xh - refh)) <= 1e-12 * np.max(np.abs(refh))
+
+
+def test_ita_zero_input():
+    p = SarParams(n_az=32, n_rg=32)
+    op = csa.CSAOperator(p)
+    X = ita.ita(op, np.zeros(op.shape), np.ones(op.shape), rule="lambda", lam=0.1, iters=3)
+    assert not np.any(X)
+
+
+def test_ita_fixed_lambda_objective_monotone():
+    """ISTA with mu <= 1/||A||^2 = 1 decreases F = 1/2||Theta(Y - GX)||^2 + lambda||X||_1 (R11, R12)."""
+    p = SarParams(n_az=64, n_rg=64)
+    op = csa.CSAOperator(p)
+    r = np.random.default_rng(2)
+    X0 = np.zeros(op.shape, complex)
+    X0.reshape(-1)[r.choice(X0.size, 30, replace=False)] = np.exp(2j * np.pi * r.random(30)) * 5
+    m = (r.random(op.shape) < 0.5).astype(float)
+    Y = m * (op.G(X0) + 0.05 * _rand(op.shape, 3))
+    for lam in (0.3, 1.0):
+        X = np.zeros(op.shape, complex)
+        F = [ita.objective_soft(op, X, Y, m, lam)]
+        for _ in range(15):
+            X = ita.ita(op, Y, m, thr="soft", rule="lambda", lam=lam, mu=1.0, iters=1, X0=X)
+            F.append(ita.objective_soft(op, X, Y, m, lam))
+        assert all(F[i + 1] <= F[i] * (1 + 1e-12) for i in range(len(F) - 1)), F
+
+
+def test_ita_support_bound_every_iteration():
+    p = SarParams(n_az=64, n_rg=64)
+    op = csa.CSAOperator(p)
+    Y = _rand(op.shape, 21)
+    m = (np.random.default_rng(1).random(op.shape) < 0.3).astype(float)
+    log = []
+    ita.ita(op, Y * m, m, thr="half", rule="k", k=25, iters=8, log=log)
+    assert all(e["support"] <= 25 for e in log)
+
+
+def test_ita_recovers_c0_support():
+    """c0 physics: 5 point targets, 50% mask, 30 dB -> exact support, wide gap."""
+    cfg = configs.get("c0")
+    prob = synth.make_problem(cfg, lambda sc, c: echo.exact_echo(c.params, sc.targets))
+    op = csa.CSAOperator(cfg.params)
+    log = []
+    X = ita.ita(op, prob.Y, prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=cfg.iters, log=log)
+    supp = set(np.flatnonzero(X).tolist())
+    assert supp == set(prob.scene.idx.tolist())
+    assert min(e["gap"] for e in log) > 1.0
+    assert log[-1]["resid2"] < log[0]["resid2"]
