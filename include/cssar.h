@@ -1,0 +1,142 @@
+/* cssar.h — C ABI of libcssar: the data-parallel hot path of fast CS-SAR imaging based on
+ * approximated observation (Fang, Xu, Zhang, Hong, Wu, arXiv 1302.3120), B200 (sm_100a).
+ *
+ * The method (PAPER.md = P:Lnnn):
+ *   Algorithm 1 / eq. 25:
+ *       X^(i+1) = E_sigma( X^(i) + mu * M( Theta o (Y_s - Theta o G(X^(i))) ) )
+ *   M = CSA matched-filter focusing chain (eq. 10, with the chirp-scaling
+ *       algorithm named at P:L243 in place of RDA), G = M^H = M^-1 the approximated
+ *       observation (eq. 11; Theorem 1), Theta the sampling mask (eq. 4,
+ *       P:L81; eq. 24), E_sigma the soft (eq. 9) or q=1/2 threshold,
+ *       sigma = lambda*mu from the k-sparsity rule or a fixed lambda.
+ *
+ * Conventions for every call:
+ *   - Arrays are complex64 (interleaved fp32 re, im; 8 bytes/sample), row-major
+ *     [n_az][n_rg]: row = azimuth line (or Doppler bin), column = range gate (or range-
+ *     frequency bin).  Frequency axes are in FFT bin order (no fftshift).
+ *   - DFTs are unitary (1/sqrt(N) per transform, "keep the throwaway consistent").
+ *   - Array pointers are DEVICE pointers, 16-byte aligned, owned by the caller (the
+ *     library never frees or retains them).  `stream` is a cudaStream_t (may be 0); all
+ *     calls are asynchronous on it unless stated otherwise.
+ *   - The mask is 1 bit per sample, row-major, LSB-first in uint32 words, each row padded
+ *     to a whole number of words (n_rg/32 words per row).  mask_bits == NULL means
+ *     Theta = all ones.  Y may hold garbage at unsampled positions (Theta is applied).
+ *   - Return value: 0 (CSSAR_OK) or a negative CSSAR_ERR_* code; no partial side effects
+ *     on argument-validation errors.
+ *   - A plan is not thread-safe: one call in flight per plan.
+ */
+#ifndef CSSAR_H_
+#define CSSAR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CSSAR_OK = 0,
+  CSSAR_ERR_INVALID_PARAMS = -1,   /* non-positive rate/velocity/range, squint != 0, pulse < 2 samples */
+  CSSAR_ERR_UNSUPPORTED_SIZE = -2, /* n_az, n_rg not powers of two in [128, 32768] / [128, 16384] */
+  CSSAR_ERR_BAD_K = -3,            /* k-rule with k < 1 or k >= n_az*n_rg */
+  CSSAR_ERR_BAD_MU = -4,           /* mu <= 0 or not finite; lambda < 0 */
+  CSSAR_ERR_ALIGNMENT = -5,        /* a pointer is NULL or not 16-byte aligned */
+  CSSAR_ERR_NONFINITE = -6,        /* NaN/Inf reached the iterate (reported when the log is read) */
+  CSSAR_ERR_CUDA = -7,             /* a CUDA runtime call failed */
+  CSSAR_ERR_WORKSPACE = -8,        /* no / too small workspace bound for cssar_ita_iterate */
+  CSSAR_ERR_NCCL = -9,             /* reserved for the multi-GPU path */
+  CSSAR_ERR_BAD_PLAN = -10         /* NULL plan or world/rank combination not supported */
+};
+
+/* SAR system parameters: the fields of Table 1 used by CSA, plus the grid.
+ * fc carrier [Hz], Kr range FM rate [Hz/s], Tr pulse duration [s], Fr range sampling
+ * rate [Hz], prf [Hz], Vr effective velocity [m/s], R_ref scene-centre slant range [m]
+ * (gate n_rg/2 <-> R_ref), squint [rad] (must be 0). */
+typedef struct {
+  double fc, Kr, Tr, Fr, prf, Vr, R_ref, squint;
+  int64_t n_az, n_rg;
+} cssar_sar_params;
+
+typedef enum { CSSAR_THR_SOFT = 1 /* q = 1, eq. 9 */, CSSAR_THR_HALF = 2 /* q = 1/2 */ } cssar_thr;
+typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 /* eq. 7 */ } cssar_rule;
+
+/* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
+ * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule. */
+typedef struct {
+  int32_t thr;      /* cssar_thr */
+  int32_t rule;     /* cssar_rule */
+  int64_t k;
+  double lambda;
+  double mu;
+  int32_t iters;
+  int32_t flags;    /* reserved, 0 */
+} cssar_ita_params;
+
+/* Per-iteration log (SPEC "SolverReport"): sigma_i = lambda_i mu_i, lambda_i,
+ * support = #{|b_i| > sigma_i} (= #nonzeros of X_(i+1)), resid2 = ||Theta(Y - G X_i)||^2. */
+typedef struct {
+  float sigma;
+  float lambda;
+  int64_t support;
+  double resid2;
+} cssar_iter_log;
+
+typedef struct cssar_plan_s* cssar_plan;
+
+/* Validate p, build the per-Doppler-bin CSA phase coefficient table (u64 fixed-point
+ * cycles) and upload it.  world/rank: 1/0 (single GPU;
+ * other values -> CSSAR_ERR_BAD_PLAN in this build).  nccl_unique_id: NULL.
+ * Allocates only small device tables (< 4 MB). Synchronous. */
+int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int rank,
+                      const void* nccl_unique_id, void* stream);
+int cssar_plan_destroy(cssar_plan plan);
+
+/* Bytes of device workspace cssar_ita_iterate needs (one complex64 array of the scene
+ * size plus a candidate buffer for the exact top-k select, ~8.5 B/sample). */
+int cssar_workspace_size(cssar_plan plan, size_t* bytes);
+/* Bind caller-owned workspace (device, 256-byte aligned).  Kept until rebound or the
+ * plan is destroyed; the caller keeps it alive. */
+int cssar_bind_workspace(cssar_plan plan, void* ws, size_t bytes);
+
+/* Y_out = Theta o G(X)   (A X, eq. 24).  X and Y_out may alias. */
+int cssar_forward(cssar_plan plan, const void* X, const uint32_t* mask_bits, void* Y_out, void* stream);
+/* X_out = M(Theta o R)   (A^H R).  R and X_out may alias. */
+int cssar_adjoint(cssar_plan plan, const void* R, const uint32_t* mask_bits, void* X_out, void* stream);
+/* X_out = M(Theta o Y): the conventional matched-filter (CSA) image of eq. 10. */
+int cssar_image(cssar_plan plan, const void* Y, const uint32_t* mask_bits, void* X_out, void* stream);
+
+/* Run `iters` ITA iterations (Algorithm 1 / eq. 25) starting from X_inout (zeros for
+ * Algorithm 1's X^(0) = 0; any X for resume).  On return X_inout = X^(iters).  Needs a
+ * bound workspace.  log_host (host array of >= iters entries) may be NULL; when given,
+ * the call copies the log back and SYNCHRONISES the stream, and reports
+ * CSSAR_ERR_NONFINITE if NaN/Inf were seen.  The iteration body is replayed as a CUDA
+ * graph captured once per (pointers, params) and cached in the plan. */
+int cssar_ita_iterate(cssar_plan plan, const void* Y, const uint32_t* mask_bits,
+                      const cssar_ita_params* prm, void* X_inout, cssar_iter_log* log_host,
+                      void* stream);
+
+/* mask_u8 (device, rows*cols bytes, nonzero = sampled) -> bit-packed mask (rows*cols/32
+ * words); cols must be a multiple of 32. */
+int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, int64_t cols, void* stream);
+
+const char* cssar_error_string(int code);
+
+/* ---- test hooks (parity of single sweeps / the select; not needed by users) ---------- */
+/* One range sweep in place on a (Doppler, range-time) array: gbody=1 -> Phi3* F Phi2* F^-1
+ * Phi1* (G body), gbody=0 -> Phi1 F Phi2 F^-1 Phi3 (M body). */
+int cssar_debug_range_sweep(cssar_plan plan, void* U, int gbody, void* stream);
+/* Unitary azimuth DFT of every column: dir = -1 forward, +1 inverse.  in/out may alias. */
+int cssar_debug_az_fft(cssar_plan plan, const void* in, void* out, int dir, void* stream);
+/* k-rule select on an arbitrary complex64 array b (n = n_az*n_rg): writes the fp32 bit
+ * pattern of the (k+1)-th largest |b|^2 (explicitly rounded re*re + im*im) and the number
+ * of entries strictly above it.  Synchronous.  Needs a bound workspace. */
+int cssar_debug_select(cssar_plan plan, const void* b, int64_t k, uint32_t* sigma2_bits_out,
+                       int64_t* above_out, void* stream);
+/* Number of full-histogram fallbacks taken by the last cssar_ita_iterate (synchronous). */
+int cssar_debug_fallbacks(cssar_plan plan, int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSSAR_H_ */

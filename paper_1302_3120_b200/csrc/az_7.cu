@@ -1,0 +1,4 @@
+#include "az.cuh"
+namespace cssar {
+template cudaError_t az_dispatch_mode<7>(int, int, const AzArgs&, cudaStream_t);
+}  // namespace cssar

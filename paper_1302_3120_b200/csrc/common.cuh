@@ -1,0 +1,134 @@
+// Device helpers: complex arithmetic, in-register radix-R DFTs, exact twiddles,
+// fixed-point CSA phase evaluation.  sm_100a only; no code shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CSSAR_DEV __device__ __forceinline__
+
+namespace cssar {
+
+CSSAR_DEV float2 operator+(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+CSSAR_DEV float2 operator-(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+CSSAR_DEV float2 operator*(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+CSSAR_DEV float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+CSSAR_DEV float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+
+// cos(2 pi o / 32), o = 0..8 (first octant plus the octant edge), correctly rounded.
+CSSAR_DEV constexpr float cos32(int o) {
+  return o == 0 ? 1.0f : o == 1 ? 0.98078528040323043f : o == 2 ? 0.92387953251128674f
+       : o == 3 ? 0.83146961230254524f : o == 4 ? 0.70710678118654752f : o == 5 ? 0.55557023301960218f
+       : o == 6 ? 0.38268343236508977f : o == 7 ? 0.19509032201612827f : 0.0f;
+}
+
+// v * exp(DIR * 2 pi i * idx / 32); idx is a compile-time constant after unrolling.
+template <int DIR>
+CSSAR_DEV float2 tw32(float2 v, int idx) {
+  idx &= 31;
+  if (idx == 0) return v;
+  if (idx == 16) return make_float2(-v.x, -v.y);
+  if (idx == 8) return DIR > 0 ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
+  if (idx == 24) return DIR > 0 ? make_float2(v.y, -v.x) : make_float2(-v.y, v.x);
+  const int q = idx >> 3, o = idx & 7;   // quadrant, offset within the quadrant
+  const float c0 = cos32(o), s0 = cos32(8 - o);
+  float c = q == 0 ? c0 : q == 1 ? -s0 : q == 2 ? -c0 : s0;
+  float s = q == 0 ? s0 : q == 1 ? c0 : q == 2 ? -s0 : -c0;
+  if (DIR < 0) s = -s;
+  return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+}
+
+CSSAR_DEV constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+template <int R>
+struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
+template <>
+struct Log2<1> { static constexpr int v = 0; };
+
+template <int R>
+CSSAR_DEV constexpr int bitrev(int i) {
+  int r = 0;
+  for (int b = 0; b < Log2<R>::v; ++b) r |= ((i >> b) & 1) << (Log2<R>::v - 1 - b);
+  return r;
+}
+
+// In-register DFT of length R (power of two, R <= 32):
+//   v[k] <- sum_n v[n] exp(DIR * 2 pi i n k / R), unscaled, natural order in and out.
+template <int R, int DIR>
+CSSAR_DEV void dft(float2 (&v)[R]) {
+  if constexpr (R == 1) return;
+  else {
+#pragma unroll
+    for (int span = R / 2; span >= 1; span >>= 1) {
+#pragma unroll
+      for (int blk = 0; blk < R; blk += 2 * span) {
+#pragma unroll
+        for (int m = 0; m < span; ++m) {
+          float2 a = v[blk + m], b = v[blk + m + span];
+          v[blk + m] = a + b;
+          v[blk + m + span] = tw32<DIR>(a - b, m * (32 / (2 * span)));
+        }
+      }
+    }
+    float2 t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = v[i];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = t[bitrev<R>(i)];
+  }
+}
+
+// exp(DIR * 2 pi i * num / den) for integers 0 <= num < den, den a power of two <= 2^24:
+// the argument 2*num/den is exact in fp32 and sincospif is accurate to ~1 ulp.
+template <int DIR>
+CSSAR_DEV float2 expi_frac(uint32_t num, uint32_t den) {
+  float s, c;
+  sincospif(2.0f * (float)num / (float)den, &s, &c);
+  return make_float2(c, DIR > 0 ? s : -s);
+}
+
+// Twiddles w^r, r = 0..R-1, with w = exp(DIR 2 pi i k / L): exact anchors w^(2^a) from
+// sincospif on the reduced integer argument, other powers as products of anchors
+// (<= log2(R)-1 roundings each).
+template <int R, int DIR>
+CSSAR_DEV void twiddle_powers(uint32_t k, uint32_t L, float2 (&w)[R]) {
+  constexpr int LR = Log2<R>::v;
+  float2 anc[LR > 0 ? LR : 1];
+#pragma unroll
+  for (int a = 0; a < LR; ++a) anc[a] = expi_frac<DIR>((k << a) & (L - 1), L);
+  w[0] = make_float2(1.f, 0.f);
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    const int low = r & (-r);           // lowest set bit
+    const int a = ilog2c(low);
+    if (r == low) w[r] = anc[a];
+    else w[r] = cmul(w[r - low], anc[a]);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Fixed-point CSA phases: each phase screen row is a
+// quadratic P(u) = C2 u^2 + C1 u + C0 in *cycles*, coefficients stored as u64 fractions
+// of a cycle (2^64 = 1 cycle).  Wrap-around u64 arithmetic is exact mod 1 cycle.
+// The phase is the top 24 bits rounded to nearest, converted exactly to fp32.
+struct Quad { uint64_t c2, c1, c0; };
+
+CSSAR_DEV uint64_t quad_eval(const Quad& q, int32_t u) {
+  uint64_t uu = (uint64_t)(int64_t)u;
+  uint64_t u2 = (uint64_t)((int64_t)u * (int64_t)u);
+  return q.c2 * u2 + q.c1 * uu + q.c0;
+}
+
+// exp(+-2 pi i P / 2^64)
+template <bool CONJ>
+CSSAR_DEV float2 phase_from_fixed(uint64_t P) {
+  uint32_t t = (uint32_t)((P + (1ull << 39)) >> 40) & 0xFFFFFFu;   // 24-bit, rounded
+  float s, c;
+  sincospif((float)t * (1.0f / 8388608.0f), &s, &c);              // pi * t / 2^23 = 2 pi t / 2^24
+  return make_float2(c, CONJ ? -s : s);
+}
+
+}  // namespace cssar

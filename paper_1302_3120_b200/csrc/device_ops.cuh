@@ -1,0 +1,64 @@
+// libcssar device kernels (sm_100a): range sweeps, azimuth sweeps (thread-block clusters +
+// DSMEM for long columns), fused residual / step / threshold epilogues, exact k-rule select.
+//
+// Hot path per ITA iteration (eq. 25, Algorithm 1):
+//   S1 az FWD_THR : X = E(b; sigma) ; F_eta                                  (G head)
+//   S2 rg <G>     : Phi3* -> F_tau -> Phi2* -> F_tau^-1 -> Phi1*              (G body)
+//   S3 az RESID   : F_eta^-1 ; r = Theta o (Y - G X) ; F_eta                  (residual)
+//   S4 rg <M>     : Phi1 -> F_tau -> Phi2 -> F_tau^-1 -> Phi3                 (M body)
+//   S5 az TAIL    : F_eta^-1 ; b = E(b; sigma) + mu dX ; |b|^2 histogram      (step)
+//   S6 select     : sigma^2 = (k+1)-th largest |b|^2 (exact radix select)     (lambda rule)
+#pragma once
+#include <cooperative_groups.h>
+#include "fft_engine.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cssar {
+
+// ------------------------------------------------------------------ elementwise pieces
+CSSAR_DEV uint32_t mag2_bits(float2 v) {
+  // |v|^2 with explicit roundings (no FMA contraction): reproducible on the host
+  return __float_as_uint(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
+}
+
+// E(b; sigma): strict survival on the fp32 |b|^2 pattern,
+// soft (eq. 9) or half (q = 1/2) shrink of the magnitude, phase preserved.
+CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
+  const uint32_t u = mag2_bits(b);
+  if (u <= s2bits) return make_float2(0.f, 0.f);
+  if (sigma == 0.f) return b;
+  const float a = sqrtf(__uint_as_float(u));
+  float f;
+  if (thr == THR_SOFT) {
+    f = 1.0f - sigma / a;
+  } else {
+    const float ratio = sigma / a;
+    const float phi = acosf(0.70710678118654752f * ratio * sqrtf(ratio));
+    f = (2.0f / 3.0f) * (1.0f + cosf(2.09439510239319549f - (2.0f / 3.0f) * phi));
+  }
+  return make_float2(b.x * f, b.y * f);
+}
+
+CSSAR_DEV uint32_t mask_bit(const uint32_t* mask, int words, int row, int col) {
+  if (!mask) return 1u;
+  return (__ldg(mask + (size_t)row * words + (col >> 5)) >> (col & 31)) & 1u;
+}
+
+// x[r] *= exp(+-2 pi i P(u0 + r S)), r < R, by exact u64 second differences
+template <int R, int S, bool CONJ>
+CSSAR_DEV void phase_apply(const Quad& q, int u0, float2* x) {
+  uint64_t P = quad_eval(q, u0);
+  uint64_t d1 = q.c2 * (uint64_t)((int64_t)2 * u0 * S + (int64_t)S * S) + q.c1 * (uint64_t)S;
+  const uint64_t d2 = q.c2 * (uint64_t)(2ll * S * S);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    x[r] = cmul(x[r], phase_from_fixed<CONJ>(P));
+    P += d1;
+    d1 += d2;
+  }
+}
+
+
+}  // namespace cssar

@@ -1,0 +1,220 @@
+// CTA-level batched FFT engine (Stockham autosort, register butterflies, SMEM exchanges).
+//
+// A CTA holds B independent transforms of length N = 2^LOGN (B*N complex64 in SMEM).
+// Each of the T threads owns E = N*B/T elements in registers.  A pass of radix R
+// processes N*B/R butterflies; thread t handles butterflies g = m*T + t, m < E/R.
+// Butterfly g -> (batch b, index j):  BMINOR (SMEM [i][b], azimuth panels): b = g % B,
+// j = g / B;  otherwise (SMEM [b][i], range rows): b = g / (N/R), j = g % (N/R).
+//
+// Stockham pass (radix R, NS = product of earlier radices), butterfly j, k = j % NS:
+//   v[r] = in[j + r N/R] * w_{NS R}^{r k};  v = DFT_R(v);  out[(j/NS) NS R + k + r NS] = v[r].
+// The first pass reads through a caller Load functor (global memory + prologue), the last
+// pass hands natural-order elements j + r N/R to a Store functor (epilogue + global
+// memory).  fft_conv() runs transform -> Mid -> inverse transform with the Mid functor
+// applied in registers between the last forward pass and the first inverse pass (they act
+// on the same element groups j + r N/R), saving two SMEM exchanges.
+//
+// SMEM bank conflicts: the writer of an exchange with NS < G (G = transform indices per
+// 128-byte wavefront) XOR-swizzles index bits [log2 NS, log2 G) with the bits above
+// log2(NS R); reader and writer agree on the swizzle of each exchange.
+#pragma once
+#include "common.cuh"
+
+namespace cssar {
+
+// ----- radix plans: log2 of the radix of each pass, and elements per thread ----------------
+CSSAR_DEV constexpr int plan_passes(int logn) { return logn <= 8 ? 2 : logn <= 10 ? 2 : 3; }
+CSSAR_DEV constexpr int plan_lr(int logn, int p) {
+  // 7:[16,8] 8:[16,16] 9:[16,32] 10:[32,32] 11:[16,8,16] 12:[16,16,16] 13:[16,32,16]
+  // 14:[32,16,32] 15:[32,32,32]
+  return logn == 7 ? (p == 0 ? 4 : 3)
+       : logn == 8 ? 4
+       : logn == 9 ? (p == 0 ? 4 : 5)
+       : logn == 10 ? 5
+       : logn == 11 ? (p == 1 ? 3 : 4)
+       : logn == 12 ? 4
+       : logn == 13 ? (p == 1 ? 5 : 4)
+       : logn == 14 ? (p == 1 ? 4 : 5)
+       : 5;
+}
+CSSAR_DEV constexpr int plan_E(int logn) {
+  return (logn == 9 || logn == 10 || logn == 13 || logn == 14 || logn == 15) ? 32 : 16;
+}
+
+template <int LOGN, int B, int T, bool BMINOR>
+struct Engine {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int P = plan_passes(LOGN);
+  static constexpr int E = plan_E(LOGN);
+  static_assert(N * B == T * E, "CTA shape must give E elements per thread");
+  static constexpr int G = BMINOR ? (B >= 16 ? 1 : 16 / B) : 16;
+
+  // radix / NS of pass p; REV = passes in reverse order (the inverse half of fft_conv)
+  template <bool REV>
+  static CSSAR_DEV constexpr int lr(int p) { return plan_lr(LOGN, REV ? P - 1 - p : p); }
+  template <bool REV>
+  static CSSAR_DEV constexpr int lns(int p) {
+    int s = 0;
+    for (int q = 0; q < p; ++q) s += lr<REV>(q);
+    return s;
+  }
+
+  template <int LNS, int LR>
+  static CSSAR_DEV int swz(int i) {
+    constexpr int NS = 1 << LNS;
+    if constexpr (NS >= G || LNS + LR >= LOGN) {
+      return i;
+    } else {
+      constexpr int mask = G / NS - 1;
+      return i ^ (((i >> (LNS + LR)) & mask) << LNS);
+    }
+  }
+  static CSSAR_DEV int addr(int b, int i) { return BMINOR ? i * B + b : b * N + i; }
+
+  template <int R>
+  static CSSAR_DEV void bj(int g, int& b, int& j) {
+    if constexpr (BMINOR) { b = g % B; j = g / B; }
+    else { b = g / (N / R); j = g % (N / R); }
+  }
+
+  // butterflies of one pass on registers v (E elements: group m at v[m*R .. m*R+R))
+  template <int LR, int LNS, int DIR>
+  static CSSAR_DEV void butterflies(float2 (&v)[E], int t) {
+    constexpr int R = 1 << LR, NS = 1 << LNS;
+#pragma unroll
+    for (int m = 0; m < E / R; ++m) {
+      int b, j;
+      bj<R>(m * T + t, b, j);
+      float2 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = v[m * R + r];
+      if constexpr (NS > 1) {
+        float2 w[R];
+        twiddle_powers<R, DIR>((uint32_t)(j & (NS - 1)), (uint32_t)(NS * R), w);
+#pragma unroll
+        for (int r = 1; r < R; ++r) x[r] = cmul(x[r], w[r]);
+      }
+      dft<R, DIR>(x);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[m * R + r] = x[r];
+    }
+  }
+
+  // write pass output (writer LR, LNS) to SMEM, swizzled for this exchange
+  template <int LR, int LNS>
+  static CSSAR_DEV void write(float2* s, const float2 (&v)[E], int t) {
+    constexpr int R = 1 << LR, NS = 1 << LNS;
+#pragma unroll
+    for (int m = 0; m < E / R; ++m) {
+      int b, j;
+      bj<R>(m * T + t, b, j);
+      const int base = (j >> LNS) * (NS * R) + (j & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[addr(b, swz<LNS, LR>(base + r * NS))] = v[m * R + r];
+    }
+  }
+
+  // read the input of a pass with radix 2^LR from SMEM written by exchange (WLR, WLNS)
+  template <int LR, int WLR, int WLNS>
+  static CSSAR_DEV void read(const float2* s, float2 (&v)[E], int t) {
+    constexpr int R = 1 << LR;
+#pragma unroll
+    for (int m = 0; m < E / R; ++m) {
+      int b, j;
+      bj<R>(m * T + t, b, j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[m * R + r] = s[addr(b, swz<WLNS, WLR>(j + r * (N / R)))];
+    }
+  }
+
+  template <int LR, class F>
+  static CSSAR_DEV void for_groups(float2 (&v)[E], int t, F&& f) {
+    constexpr int R = 1 << LR;
+#pragma unroll
+    for (int m = 0; m < E / R; ++m) {
+      int b, j;
+      bj<R>(m * T + t, b, j);
+      f(b, j, &v[m * R]);
+    }
+  }
+
+  // Passes p = P0 .. P-1 of a transform whose first pass input is already in registers.
+  // On return the last pass output (natural order, groups j + r N/R_last) is in v.
+  template <int DIR, bool REV, int p>
+  static CSSAR_DEV void passes_from(float2* s, float2 (&v)[E], int t) {
+    constexpr int LR = lr<REV>(p), LNS = lns<REV>(p);
+    butterflies<LR, LNS, DIR>(v, t);
+    if constexpr (p + 1 < P) {
+      __syncthreads();                 // everyone finished reading the previous exchange
+      write<LR, LNS>(s, v, t);
+      __syncthreads();
+      read<lr<REV>(p + 1), LR, LNS>(s, v, t);
+      passes_from<DIR, REV, p + 1>(s, v, t);
+    }
+  }
+
+  // Load functor: ld(b, j, x) fills x[r] = input element (b, j + r N/R0), R0 = first radix.
+  // Store functor: st(b, j, x) consumes output elements (b, j + r N/R_last).
+  template <int DIR, class Load, class Store>
+  static CSSAR_DEV void run(float2* s, Load&& ld, Store&& st) {
+    const int t = threadIdx.x;
+    float2 v[E];
+    for_groups<lr<false>(0)>(v, t, ld);
+    passes_from<DIR, false, 0>(s, v, t);
+    for_groups<lr<false>(P - 1)>(v, t, st);
+  }
+
+  // transform(DIR) -> mid -> transform(-DIR), mid acting on natural-order groups in registers
+  template <int DIR, class Load, class Mid, class Store>
+  static CSSAR_DEV void conv(float2* s, Load&& ld, Mid&& mid, Store&& st) {
+    const int t = threadIdx.x;
+    float2 v[E];
+    for_groups<lr<false>(0)>(v, t, ld);
+    passes_from<DIR, false, 0>(s, v, t);
+    for_groups<lr<false>(P - 1)>(v, t, mid);
+    passes_from<-DIR, true, 0>(s, v, t);
+    for_groups<lr<true>(P - 1)>(v, t, st);
+  }
+
+  // run() without the Store: the natural-order output groups stay in v (for cluster kernels)
+  template <int DIR, class Load>
+  static CSSAR_DEV void run_keep(float2* s, float2 (&v)[E], Load&& ld) {
+    const int t = threadIdx.x;
+    for_groups<lr<false>(0)>(v, t, ld);
+    passes_from<DIR, false, 0>(s, v, t);
+  }
+
+  // write the natural-order output groups of the last pass (radix of pass P-1) unswizzled
+  // to s[addr(b, i)]; brackets the write with barriers (other threads may still be reading
+  // the last exchange, and readers of the result must wait for every writer)
+  static CSSAR_DEV void store_natural(float2* s, const float2 (&v)[E]) {
+    const int t = threadIdx.x;
+    constexpr int LR = lr<false>(P - 1), R = 1 << LR;
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E / R; ++m) {
+      int b, j;
+      bj<R>(m * T + t, b, j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[addr(b, j + r * (N / R))] = v[m * R + r];
+    }
+    __syncthreads();
+  }
+
+  // Same as run(), but the first pass reads its input from SMEM in natural order
+  // (s[addr(b, i)], unswizzled) — used after a cluster scatter.
+  template <int DIR, class Store>
+  static CSSAR_DEV void run_from_smem(float2* s, Store&& st) {
+    const int t = threadIdx.x;
+    float2 v[E];
+    constexpr int LR0 = lr<false>(0), R0 = 1 << LR0;
+    for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = s[addr(b, j + r * (N / R0))];
+    });
+    passes_from<DIR, false, 0>(s, v, t);
+    for_groups<lr<false>(P - 1)>(v, t, st);
+  }
+};
+
+}  // namespace cssar

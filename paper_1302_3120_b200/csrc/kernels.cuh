@@ -1,0 +1,93 @@
+// Kernel declarations and device-side shared structures for libcssar.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace cssar {
+
+// Per-Doppler-row CSA phase coefficients (u64 fixed-point cycles), DESIGN.md "Phase generation".
+//   q[0] = Phi1 (chirp scaling)            in u = j - n_rg/2
+//   q[1] = Phi2 (range compr. + bulk RCMC) in signed range-frequency bin l'
+//   q[2] = Phi3 (azimuth compr. + residual) in u = j - n_rg/2
+struct RowCoef { Quad q[3]; };
+
+enum Thr : int { THR_SOFT = 1, THR_HALF = 2 };
+enum Rule : int { RULE_K = 1, RULE_LAMBDA = 2 };
+
+constexpr int HIST_BITS = 11;                  // top bits of the 31-bit |b|^2 pattern
+constexpr int HIST_BINS = 1 << HIST_BITS;      // 2048 bins, 8 per octave of |b|^2
+constexpr int HIST_SHIFT = 31 - HIST_BITS;     // 20
+constexpr int FLOOR_MARGIN = 24;               // bins below the last sigma^2 bin still counted
+constexpr int CAND_MARGIN = 2;                 // candidate window half-width (bins)
+
+// Device-resident solver state (one per plan); no host round trip inside the loop.
+struct SelState {
+  uint32_t sigma2_bits;     // threshold sigma^2 (fp32 bit pattern) used by E(.)
+  float sigma;              // sqrt(sigma^2) (shrink amount)
+  float sigma_fixed;        // fixed-lambda rule: sigma = lambda mu (soft) / half jump point
+  uint32_t sigma2_fixed_bits;
+  int32_t floor_bin;        // TAIL histograms only bins >= floor_bin
+  int32_t cand_lo, cand_hi; // TAIL writes candidates with bin in [lo, hi]
+  uint32_t cand_count;
+  uint32_t cand_overflow;
+  int32_t need_full;        // 1: coarse select failed -> full-histogram fallback
+  int32_t target_bin;
+  uint32_t target_rank;     // 0-based rank from the top inside target_bin
+  uint64_t above_count;     // # elements in bins above target_bin
+  int32_t iter;             // iteration counter (log index)
+  uint32_t nonfinite;
+  double resid2;            // ||Theta(Y - G X)||^2 of the current iteration
+  unsigned long long support_fixed;
+  int32_t fallbacks;        // # iterations that needed the full-histogram fallback
+};
+
+struct IterLogDev { float sigma; float lam; long long support; double resid2; };
+
+struct AzArgs {
+  const float2* in;
+  float2* out;
+  const float2* Y;
+  const uint32_t* mask;     // bit-packed, mask_words per row; nullptr = all ones
+  float2* b;                // TAIL / THR: state array
+  SelState* st;
+  uint32_t* hist;           // HIST_BINS
+  uint32_t* cand;           // candidate |b|^2 patterns
+  uint32_t cand_cap;
+  int n_rg;
+  int mask_words;
+  int thr;
+  int rule;
+  float mu;
+  float scale;              // 1/sqrt(n_az)
+};
+
+struct RgArgs {
+  float2* data;
+  const RowCoef* coef;
+  int row_base;             // global Doppler row of data row 0
+  float scale;              // 1/n_rg
+};
+
+enum AzMode : int {
+  AZ_FWD_PLAIN = 0,   // F_eta x
+  AZ_FWD_MASK = 1,    // F_eta (Theta o r)
+  AZ_FWD_THR = 2,     // F_eta E(b; sigma)                          (S1)
+  AZ_INV_PLAIN = 3,   // F_eta^-1 u
+  AZ_INV_MASK = 4,    // Theta o F_eta^-1 u
+  AZ_RESID = 5,       // F_eta Theta o (Y - F_eta^-1 u)               (S3)
+  AZ_TAIL = 6,        // b <- E(b; sigma) + mu F_eta^-1 u, histogram  (S5)
+};
+
+// host-side launchers (kernels.cu)
+cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s);
+cudaError_t launch_az(int log_naz, int mode, int n_rg_local, const AzArgs& a, cudaStream_t s);
+cudaError_t launch_select(int n_threads_hint, float2* b, long long n, long long k, int rule, int thr, float mu,
+                          SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand, uint32_t cand_cap,
+                          IterLogDev* log, int log_cap, cudaStream_t s);
+cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,
+                              cudaStream_t s);
+cudaError_t launch_finalize(float2* b, long long n, int thr, const SelState* st, cudaStream_t s);
+cudaError_t launch_pack_mask(const uint8_t* m, uint32_t* bits, long long rows, long long cols, cudaStream_t s);
+
+}  // namespace cssar

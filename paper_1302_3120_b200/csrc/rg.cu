@@ -1,0 +1,72 @@
+// Range sweeps (S2 G body, S4 M body): one or more range lines per CTA.
+#include "device_ops.cuh"
+
+namespace cssar {
+
+// ------------------------------------------------------------------ range sweep
+template <int LOGN>
+struct RgCfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int E = plan_E(LOGN);
+  static constexpr int T = LOGN >= 14 ? 512 : 256;
+  static constexpr int B = (T * E) / N > 0 ? (T * E) / N : 1;
+  static constexpr size_t SMEM = sizeof(float2) * N * B;
+};
+
+// GBODY: Phi3* -> F -> Phi2* -> F^-1 -> Phi1*  (inverse of the focusing steps)
+// else : Phi1  -> F -> Phi2  -> F^-1 -> Phi3   (CSA focusing body)
+template <int LOGN, bool GBODY>
+__global__ void __launch_bounds__(RgCfg<LOGN>::T) rg_sweep_kernel(const RgArgs a) {
+  using C = RgCfg<LOGN>;
+  using En = Engine<LOGN, C::B, C::T, false>;
+  constexpr int N = C::N;
+  constexpr int R0 = 1 << En::template lr<false>(0);
+  constexpr int RL = 1 << En::template lr<false>(En::P - 1);
+  extern __shared__ float4 smem4[];
+  float2* s = reinterpret_cast<float2*>(smem4);
+  const int row0 = blockIdx.x * C::B;
+  float2* __restrict__ data = a.data;
+
+  auto ld = [&](int b, int j, float2* x) {
+    const float2* src = data + (size_t)(row0 + b) * N;
+#pragma unroll
+    for (int r = 0; r < R0; ++r) x[r] = src[j + r * (N / R0)];
+    const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
+    phase_apply<R0, N / R0, GBODY>(q, j - N / 2, x);
+  };
+  auto mid = [&](int b, int j, float2* x) {
+    const Quad q = a.coef[a.row_base + row0 + b].q[1];
+    // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
+    phase_apply<RL / 2, N / RL, GBODY>(q, j, x);
+    phase_apply<RL / 2, N / RL, GBODY>(q, j - N / 2, x + RL / 2);
+  };
+  auto st = [&](int b, int j, float2* x) {
+    const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
+    phase_apply<R0, N / R0, GBODY>(q, j - N / 2, x);
+    float2* dst = data + (size_t)(row0 + b) * N;
+#pragma unroll
+    for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r] * a.scale;
+  };
+  En::template conv<-1>(s, ld, mid, st);
+}
+
+template <int LOGN, bool GB>
+static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
+  using C = RgCfg<LOGN>;
+  auto k = rg_sweep_kernel<LOGN, GB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  k<<<n_rows / C::B, C::T, C::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s) {
+#define RG_CASE(L) case L: return gbody ? rg_launch<L, true>(n_rows, a, s) : rg_launch<L, false>(n_rows, a, s);
+  switch (log_nrg) {
+    RG_CASE(7) RG_CASE(8) RG_CASE(9) RG_CASE(10) RG_CASE(11) RG_CASE(12) RG_CASE(13) RG_CASE(14)
+    default: return cudaErrorInvalidValue;
+  }
+#undef RG_CASE
+}
+
+}  // namespace cssar

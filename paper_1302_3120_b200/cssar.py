@@ -1,0 +1,221 @@
+"""Thin ctypes binding of libcssar (include/cssar.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; PyTorch supplies device memory and
+streams.  There is no CPU fallback: if libcssar.so is missing or the GPU is absent, the
+calls raise.
+"""
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcssar.so")
+
+CSSAR_THR_SOFT, CSSAR_THR_HALF = 1, 2
+CSSAR_RULE_KSPARSE, CSSAR_RULE_FIXED_LAMBDA = 1, 2
+
+ERRORS = {
+    -1: "CSSAR_ERR_INVALID_PARAMS", -2: "CSSAR_ERR_UNSUPPORTED_SIZE", -3: "CSSAR_ERR_BAD_K",
+    -4: "CSSAR_ERR_BAD_MU", -5: "CSSAR_ERR_ALIGNMENT", -6: "CSSAR_ERR_NONFINITE", -7: "CSSAR_ERR_CUDA",
+    -8: "CSSAR_ERR_WORKSPACE", -9: "CSSAR_ERR_NCCL", -10: "CSSAR_ERR_BAD_PLAN",
+}
+
+# every symbol include/cssar.h declares
+SYMBOLS = [
+    "cssar_plan_create", "cssar_plan_destroy", "cssar_workspace_size", "cssar_bind_workspace",
+    "cssar_forward", "cssar_adjoint", "cssar_image", "cssar_ita_iterate", "cssar_pack_mask",
+    "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
+    "cssar_debug_fallbacks",
+]
+
+
+class CssarError(RuntimeError):
+    def __init__(self, code, what):
+        super().__init__(f"{what}: {ERRORS.get(code, code)} ({code})")
+        self.code = code
+
+
+class SarParamsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("fc", "Kr", "Tr", "Fr", "prf", "Vr", "R_ref", "squint")] + \
+               [("n_az", ctypes.c_int64), ("n_rg", ctypes.c_int64)]
+
+
+class ItaParamsC(ctypes.Structure):
+    _fields_ = [("thr", ctypes.c_int32), ("rule", ctypes.c_int32), ("k", ctypes.c_int64),
+                ("lam", ctypes.c_double), ("mu", ctypes.c_double), ("iters", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
+
+
+class IterLogC(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_float), ("lam", ctypes.c_float), ("support", ctypes.c_int64),
+                ("resid2", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libcssar.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, V, I, I64, U32P = ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint32)
+    lib.cssar_plan_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SarParamsC), I, I, V, V]
+    lib.cssar_plan_destroy.argtypes = [P]
+    lib.cssar_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
+    lib.cssar_bind_workspace.argtypes = [P, V, ctypes.c_size_t]
+    for f in ("cssar_forward", "cssar_adjoint", "cssar_image"):
+        getattr(lib, f).argtypes = [P, V, V, V, V]
+    lib.cssar_ita_iterate.argtypes = [P, V, V, ctypes.POINTER(ItaParamsC), V, ctypes.POINTER(IterLogC), V]
+    lib.cssar_pack_mask.argtypes = [V, V, I64, I64, V]
+    lib.cssar_error_string.argtypes = [I]
+    lib.cssar_error_string.restype = ctypes.c_char_p
+    lib.cssar_debug_range_sweep.argtypes = [P, V, I, V]
+    lib.cssar_debug_az_fft.argtypes = [P, V, V, I, V]
+    lib.cssar_debug_select.argtypes = [P, V, I64, U32P, ctypes.POINTER(ctypes.c_int64), V]
+    lib.cssar_debug_fallbacks.argtypes = [P, ctypes.POINTER(ctypes.c_int32), V]
+    for s in SYMBOLS:
+        if s != "cssar_error_string":
+            getattr(lib, s).restype = I
+    _lib = lib
+    return lib
+
+
+def _check(code, what):
+    if code != 0:
+        raise CssarError(code, what)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libcssar takes device tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _params_c(p):
+    return SarParamsC(p.fc, p.Kr, p.Tr, p.Fr, p.prf, p.Vr, p.R_ref, p.squint, int(p.n_az), int(p.n_rg))
+
+
+def pack_mask(mask_u8, stream=None):
+    """uint8/bool (n_az, n_rg) device tensor -> bit-packed int32 tensor (n_az, n_rg/32)."""
+    lib = load_library()
+    m = mask_u8.to(torch.uint8).contiguous()
+    rows, cols = m.shape
+    bits = torch.empty((rows, cols // 32), dtype=torch.int32, device=m.device)
+    _check(lib.cssar_pack_mask(_ptr(m), _ptr(bits), rows, cols, _stream(stream)), "cssar_pack_mask")
+    return bits
+
+
+class Plan:
+    """cssar_plan: SAR parameters -> phase-coefficient table; operator calls and ITA."""
+
+    def __init__(self, params, stream=None, workspace=True):
+        self.lib = load_library()
+        self.params = params
+        self.shape = (int(params.n_az), int(params.n_rg))
+        h = ctypes.c_void_p()
+        pc = _params_c(params)
+        _check(self.lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(pc), 1, 0, None, _stream(stream)),
+               "cssar_plan_create")
+        self.h = h
+        self.ws = None
+        if workspace:
+            self.bind_workspace()
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.cssar_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_size(self):
+        n = ctypes.c_size_t()
+        _check(self.lib.cssar_workspace_size(self.h, ctypes.byref(n)), "cssar_workspace_size")
+        return n.value
+
+    def bind_workspace(self, ws=None):
+        nbytes = self.workspace_size()
+        if ws is None:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        _check(self.lib.cssar_bind_workspace(self.h, _ptr(ws), ws.numel()), "cssar_bind_workspace")
+        self.ws = ws
+
+    def _out(self, out):
+        return torch.empty(self.shape, dtype=torch.complex64, device="cuda") if out is None else out
+
+    def forward(self, X, mask_bits=None, out=None, stream=None):
+        """A X = Theta o G(X)."""
+        out = self._out(out)
+        _check(self.lib.cssar_forward(self.h, _ptr(X), _ptr(mask_bits), _ptr(out), _stream(stream)), "cssar_forward")
+        return out
+
+    def adjoint(self, R, mask_bits=None, out=None, stream=None):
+        """A^H R = M(Theta o R)."""
+        out = self._out(out)
+        _check(self.lib.cssar_adjoint(self.h, _ptr(R), _ptr(mask_bits), _ptr(out), _stream(stream)), "cssar_adjoint")
+        return out
+
+    def image(self, Y, mask_bits=None, out=None, stream=None):
+        """Matched-filter (CSA) image M(Theta o Y), eq. 10."""
+        out = self._out(out)
+        _check(self.lib.cssar_image(self.h, _ptr(Y), _ptr(mask_bits), _ptr(out), _stream(stream)), "cssar_image")
+        return out
+
+    def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
+                    log=False, stream=None):
+        """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X."""
+        if X is None:
+            X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
+        prm = ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
+                         CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
+                         int(k), float(lam), float(mu), int(iters), 0)
+        logbuf = (IterLogC * max(1, iters))() if log else None
+        rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
+                                        logbuf if log else None, _stream(stream))
+        _check(rc, "cssar_ita_iterate")
+        if log:
+            entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2)
+                       for e in list(logbuf)[:iters]]
+            return X, entries
+        return X
+
+    # ---- test hooks
+    def debug_range_sweep(self, U, gbody, stream=None):
+        _check(self.lib.cssar_debug_range_sweep(self.h, _ptr(U), int(gbody), _stream(stream)), "range_sweep")
+        return U
+
+    def debug_az_fft(self, inp, out=None, dir=-1, stream=None):
+        out = self._out(out)
+        _check(self.lib.cssar_debug_az_fft(self.h, _ptr(inp), _ptr(out), int(dir), _stream(stream)), "az_fft")
+        return out
+
+    def debug_select(self, b, k, stream=None):
+        s2 = ctypes.c_uint32()
+        above = ctypes.c_int64()
+        _check(self.lib.cssar_debug_select(self.h, _ptr(b), int(k), ctypes.byref(s2), ctypes.byref(above),
+                                           _stream(stream)), "select")
+        return s2.value, above.value
+
+    def debug_fallbacks(self, stream=None):
+        v = ctypes.c_int32()
+        _check(self.lib.cssar_debug_fallbacks(self.h, ctypes.byref(v), _stream(stream)), "fallbacks")
+        return v.value
