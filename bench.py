@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""Benchmark of the ITA hot path (one step = one ITA iteration S1..S6 over the whole scene).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl cssar|reference]
+
+Workload (BASELINE.json configs[3], the largest scene the metric's 1..8-GPU runs use that
+fits one GPU): c3, 8192 x 8192 complex64, 1% Rayleigh clutter + 500 bright targets, 60%
+azimuth-line mask, 15 dB, soft threshold, k-rule k = 671589, mu = 1.  Synthetic inputs
+from inputs/ (seeded), echo Y = Theta o (G(X_true) + noise) generated with the library's
+own forward operator (P:L47 inverse-focusing simulation); arrays are 512 MiB each, larger
+than L2 (126 MB), so no L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  value = complex samples * iterations / s over all ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_SAMPLE = {  # algorithmic HBM bytes per sample per launch
+    "S1_az_head": 16.0, "S2_rg_G": 16.0, "S3_az_resid": 24.125, "S4_rg_M": 16.0, "S5_az_tail": 24.0,
+    "S6_select": 0.0,
+}
+ITER_BYTES_PER_SAMPLE = 96.125     # k-rule, SURVEY.md 8(a)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="cssar", choices=["cssar", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.index)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 8]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+def make_problem_gpu(cfg, plan, seed_offset=0):
+    """Seeded c-config inputs on the device; echo via the library's forward operator."""
+    import dataclasses
+    import numpy as np
+    import torch
+    from inputs import synth
+    from paper_1302_3120_b200 import pack_mask
+    if seed_offset:
+        cfg = dataclasses.replace(cfg, seed=cfg.seed + 1000 * seed_offset)
+    p = cfg.params
+    sc = synth.make_scene(cfg)
+    X = torch.zeros((p.n_az, p.n_rg), dtype=torch.complex64, device="cuda")
+    X.view(-1)[torch.from_numpy(sc.idx).cuda()] = torch.from_numpy(sc.val.astype(np.complex64)).cuda()
+    mask = torch.from_numpy(synth.make_mask(cfg)).cuda()
+    mb = pack_mask(mask.to(torch.uint8))
+    Yc = plan.forward(X, None)
+    sig = (Yc.abs() ** 2)[mask].mean()
+    s2 = sig / 10.0 ** (cfg.snr_db / 10.0)
+    noise = torch.from_numpy(synth.noise_unit(cfg, dtype=np.complex64)).cuda()
+    Y = torch.where(mask, Yc + torch.sqrt(s2) * noise, torch.zeros_like(Yc))
+    del Yc, noise, X
+    torch.cuda.synchronize()
+    return Y.contiguous(), mb, mask, sc
+
+
+def cpu_baseline(cfg_name, n_az, n_rg, iters):
+    """The fp64 oracle (as it stands) timed on this host on a bounded sample of the workload."""
+    import dataclasses
+    import numpy as np
+    from inputs import configs, synth
+    from oracle import csa, echo, ita
+    base = configs.get(cfg_name)
+    cfg = configs.with_grid(base, n_az, n_rg)
+    sc = synth.make_scene(cfg)
+    cfg = dataclasses.replace(cfg, k=int(sc.idx.size))
+    op = csa.CSAOperator(cfg.params)
+    prob = synth.make_problem(cfg, lambda s, c: echo.inverse_csa_echo(op, s.dense()))
+    Y = prob.Y.astype(np.complex128)
+    ita.ita(op, Y, prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=1)   # warm (phase screens)
+    t0 = time.perf_counter()
+    ita.ita(op, Y, prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=iters)
+    dt = time.perf_counter() - t0
+    return dict(value=n_az * n_rg * iters / dt, unit="samples*it/s", cores=len(os.sched_getaffinity(0)),
+                kind="oracle", seconds=dt,
+                sample=f"{cfg_name} recipe on a {n_az}x{n_rg} grid (k = {cfg.k}), {iters} ITA iteration(s), "
+                       f"fp64 numpy/scipy.fft (workers = all cores)")
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, each step one ITA iteration on a bounded
+    sample of the workload (c3 recipe on a 1024 x 2048 grid)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import dataclasses
+    import numpy as np
+    from inputs import configs, synth
+    from oracle import csa, echo, ita
+    n_az, n_rg = 1024, 2048
+    cfg = configs.with_grid(configs.get(args.config), n_az, n_rg)
+    sc = synth.make_scene(cfg)
+    cfg = dataclasses.replace(cfg, k=int(sc.idx.size))
+    op = csa.CSAOperator(cfg.params)
+    prob = synth.make_problem(cfg, lambda s, c: echo.inverse_csa_echo(op, s.dense()))
+    Y = prob.Y.astype(np.complex128)
+    X = np.zeros_like(Y)
+    for _ in range(args.warmup):
+        X = ita.ita(op, Y, prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=1, X0=X)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        X = ita.ita(op, Y, prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=1, X0=X)
+    dt = time.perf_counter() - t0
+    value = n_az * n_rg * args.steps / dt
+    cores = len(os.sched_getaffinity(0))
+    sample = f"{args.config} recipe on a {n_az}x{n_rg} grid (k = {cfg.k}), one ITA iteration per step"
+    line = {
+        "impl": "reference", "metric": "ITA complex samples*iterations/s", "value": value, "unit": "samples*it/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (bounded sample {n_az}x{n_rg})", "iters_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "samples*it/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "samples*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from inputs import configs
+    from paper_1302_3120_b200 import Plan
+    from paper_1302_3120_b200.cssar import STAGES
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.config)
+    p = cfg.params
+    n = p.n_az * p.n_rg
+    plan = Plan(p)
+    # weak scaling: each rank reconstructs its own scene (independent seeds) — see DESIGN.md
+    Y, mb, mask, sc = make_problem_gpu(cfg, plan, seed_offset=rank)
+    X = torch.zeros_like(Y)
+    kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    plan.ita_iterate(Y, mb, X=X, iters=args.warmup, **kw)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    plan.ita_iterate(Y, mb, X=X, iters=args.steps, **kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * n * args.steps / (ms * 1e-3)
+    it_s = args.steps / (ms * 1e-3)
+    peak, peak_kind = peaks()
+
+    # per-step breakdown (CUDA events on the launch stream inside the library)
+    stages = None
+    roof = None
+    if not args.no_profile:
+        kp = max(3, min(args.steps, 30))
+        plan.ita_iterate(Y, mb, X=X, iters=kp, profile_stages=True, **kw)
+        st_ms, it_meas = plan.stage_times()
+        stages = {k: v / it_meas for k, v in st_ms.items()}
+        dom = max((s for s in STAGES if s != "S6_select"), key=lambda s: stages[s])
+        tb = BYTES_PER_SAMPLE[dom] * n
+        achieved = tb / (stages[dom] * 1e-3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": tb, "avg_launch_ms": stages[dom]}
+
+    iter_ach = ITER_BYTES_PER_SAMPLE * n * it_s / 1e9
+    line = {
+        "metric": "ITA complex samples*iterations/s (HBM roofline fraction alongside)",
+        "value": value, "unit": "samples*it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "it_per_s": it_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {p.n_az}x{p.n_rg} complex64, {cfg.scene} scene, {cfg.mask} mask "
+                               f"{cfg.rate}, SNR {cfg.snr_db} dB, {cfg.thr} threshold, k = {cfg.k}, mu = {cfg.mu}",
+                   "n_az": p.n_az, "n_rg": p.n_rg, "k": cfg.k, "l2": "inputs larger than L2 (512 MiB arrays)",
+                   "parallelism": "single" if world == 1 else f"replicas{world} (independent scenes per GPU)"},
+        "roofline": roof,
+        "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak, "unit": "GB/s",
+                               "frac": iter_ach / peak, "bytes_per_sample": ITER_BYTES_PER_SAMPLE},
+        "stages_ms": stages,
+        "gpu_launches": args.steps * (10 if cfg.rule == "k" else 6) + 2,
+        "clocks": clocks,
+    }
+
+    if rank == 0 and not args.no_e2e:
+        # end to end through the public API: pinned host Y + mask -> device -> full solve -> host X
+        Yh = Y.cpu().pin_memory()
+        mbh = mb.cpu().pin_memory()
+        Xh = torch.empty_like(Yh).pin_memory()
+        iters = cfg.iters
+        plan.solve_host(Yh, mbh, out_host=Xh, iters=iters, **kw)      # warm (graph capture for new X)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.solve_host(Yh, mbh, out_host=Xh, iters=iters, **kw)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        h2d = Yh.numel() * 8 + mbh.numel() * 4
+        d2h = Xh.numel() * 8
+        line["e2e"] = {"value": n * iters / dt, "unit": "samples*it/s", "h2d_bytes_per_step": h2d / iters,
+                       "d2h_bytes_per_step": d2h / iters, "solve_iters": iters,
+                       "note": "one full reconstruction (config iteration count) per call; copies once per solve"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, 4096, 4096, 2)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -61,6 +61,11 @@ typedef struct {
 typedef enum { CSSAR_THR_SOFT = 1 /* q = 1, eq. 9 */, CSSAR_THR_HALF = 2 /* q = 1/2 */ } cssar_thr;
 typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 /* eq. 7 */ } cssar_rule;
 
+/* flags: CSSAR_FLAG_PROFILE_STAGES launches the iteration body directly (no graph) with CUDA
+ * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
+ * accumulates per-step device time (read with cssar_stage_times). */
+enum { CSSAR_FLAG_PROFILE_STAGES = 1 };
+
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
  * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule. */
 typedef struct {
@@ -70,7 +75,7 @@ typedef struct {
   double lambda;
   double mu;
   int32_t iters;
-  int32_t flags;    /* reserved, 0 */
+  int32_t flags;    /* CSSAR_FLAG_* bits; 0 = graph-replayed loop */
 } cssar_ita_params;
 
 /* Per-iteration log (SPEC "SolverReport"): sigma_i = lambda_i mu_i, lambda_i,
@@ -133,6 +138,11 @@ int cssar_debug_az_fft(cssar_plan plan, const void* in, void* out, int dir, void
  * of entries strictly above it.  Synchronous.  Needs a bound workspace. */
 int cssar_debug_select(cssar_plan plan, const void* b, int64_t k, uint32_t* sigma2_bits_out,
                        int64_t* above_out, void* stream);
+/* Per-step device time accumulated by the last CSSAR_FLAG_PROFILE_STAGES run: ms_out[6] =
+ * total milliseconds of S1 (az head), S2 (G range body), S3 (az residual), S4 (M range
+ * body), S5 (az tail), S6 (select); iters_out = iterations measured.  Host-only call. */
+int cssar_stage_times(cssar_plan plan, double* ms_out, int32_t* iters_out);
+
 /* Number of full-histogram fallbacks taken by the last cssar_ita_iterate (synchronous). */
 int cssar_debug_fallbacks(cssar_plan plan, int32_t* out, void* stream);
 

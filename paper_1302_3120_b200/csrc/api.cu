@@ -51,6 +51,10 @@ struct cssar_plan_s {
   cudaGraphExec_t gexec = nullptr;
   GraphKey gkey{};
   bool ghave = false;
+  // per-step profiling (CSSAR_FLAG_PROFILE_STAGES)
+  cudaEvent_t ev[7] = {};
+  double stage_ms[6] = {};
+  int stage_iters = 0;
 };
 
 namespace {
@@ -169,7 +173,8 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
 
 // one ITA iteration (S1..S6) on stream s
 int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const cssar_ita_params& prm, void* X,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool prof = false) {
+#define MARK(i) do { if (prof) CUDA_TRY(cudaEventRecord(pl->ev[i], s)); } while (0)
   AzArgs a{};
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
@@ -185,24 +190,32 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.mask = mask;
   float2* b = (float2*)X;
   RgArgs r{pl->U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg)};
+  MARK(0);
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
   a.in = b;
   a.out = pl->U;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_THR, a.n_rg, a, s));
+  MARK(1);
   // S2: G body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
+  MARK(2);
   // S3: F_eta^-1 ; r = Theta o (Y - G X_i) ; F_eta
   a.in = pl->U;
   a.out = pl->U;
   CUDA_TRY(launch_az(pl->log_naz, AZ_RESID, a.n_rg, a, s));
+  MARK(3);
   // S4: M body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
+  MARK(4);
   // S5: F_eta^-1 ; b_i = X_i + mu dX ; |b|^2 histogram + candidates
   a.b = b;
   CUDA_TRY(launch_az(pl->log_naz, AZ_TAIL, a.n_rg, a, s));
+  MARK(5);
   // S6: sigma_i (k-rule select or fixed lambda)
   CUDA_TRY(launch_select(pl->sm_count, b, pl->n, prm.k, prm.rule, prm.thr, (float)prm.mu, pl->d_st, pl->d_hist,
                          pl->d_hist_full, pl->cand, pl->cand_cap, pl->d_log, kLogCap, s));
+  MARK(6);
+#undef MARK
   return CSSAR_OK;
 }
 
@@ -261,6 +274,11 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
+  for (int i = 0; i < 7; ++i) {
+    if (cudaEventCreate(&pl->ev[i]) == cudaSuccess) continue;
+    cssar_plan_destroy(pl);
+    return CSSAR_ERR_CUDA;
+  }
   *out = pl;
   return CSSAR_OK;
 }
@@ -269,6 +287,8 @@ int cssar_plan_destroy(cssar_plan pl) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
+  for (int i = 0; i < 7; ++i)
+    if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
   cudaFree(pl->d_coef);
   cudaFree(pl->d_st);
   cudaFree(pl->d_hist);
@@ -334,7 +354,22 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   cudaStream_t s = (cudaStream_t)stream;
   const float sigma_fixed = prm->rule == CSSAR_RULE_FIXED_LAMBDA ? (float)fixed_sigma(*prm) : 0.f;
   CUDA_TRY(launch_init_state(pl->d_st, pl->d_hist, pl->d_hist_full, prm->thr, sigma_fixed, s));
-  if (prm->iters > 0) {
+  const bool prof = (prm->flags & CSSAR_FLAG_PROFILE_STAGES) != 0;
+  if (prof) {
+    for (int i = 0; i < 6; ++i) pl->stage_ms[i] = 0.0;
+    pl->stage_iters = 0;
+    for (int it = 0; it < prm->iters; ++it) {
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, true);
+      if (rc != CSSAR_OK) return rc;
+      CUDA_TRY(cudaEventSynchronize(pl->ev[6]));
+      for (int i = 0; i < 6; ++i) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, pl->ev[i], pl->ev[i + 1]));
+        pl->stage_ms[i] += ms;
+      }
+      pl->stage_iters += 1;
+    }
+  } else if (prm->iters > 0) {
     GraphKey key{Y, mask_bits, X_inout, prm->thr, prm->rule, prm->rule == CSSAR_RULE_KSPARSE ? prm->k : 0,
                  prm->lambda, prm->mu};
     if (!pl->ghave || !(pl->gkey == key)) {
@@ -418,6 +453,13 @@ int cssar_debug_select(cssar_plan pl, const void* b, int64_t k, uint32_t* sigma2
   CUDA_TRY(cudaStreamSynchronize(s));
   if (sigma2_bits_out) *sigma2_bits_out = st.sigma2_bits;
   if (above_out) *above_out = e.support;
+  return CSSAR_OK;
+}
+
+int cssar_stage_times(cssar_plan pl, double* ms_out, int32_t* iters_out) {
+  if (!pl || !ms_out) return CSSAR_ERR_BAD_PLAN;
+  for (int i = 0; i < 6; ++i) ms_out[i] = pl->stage_ms[i];
+  if (iters_out) *iters_out = pl->stage_iters;
   return CSSAR_OK;
 }
 

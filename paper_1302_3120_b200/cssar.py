@@ -26,8 +26,10 @@ SYMBOLS = [
     "cssar_plan_create", "cssar_plan_destroy", "cssar_workspace_size", "cssar_bind_workspace",
     "cssar_forward", "cssar_adjoint", "cssar_image", "cssar_ita_iterate", "cssar_pack_mask",
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
-    "cssar_debug_fallbacks",
+    "cssar_debug_fallbacks", "cssar_stage_times",
 ]
+CSSAR_FLAG_PROFILE_STAGES = 1
+STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
 
 
 class CssarError(RuntimeError):
@@ -78,6 +80,7 @@ def load_library(path=LIB_PATH):
     lib.cssar_debug_az_fft.argtypes = [P, V, V, I, V]
     lib.cssar_debug_select.argtypes = [P, V, I64, U32P, ctypes.POINTER(ctypes.c_int64), V]
     lib.cssar_debug_fallbacks.argtypes = [P, ctypes.POINTER(ctypes.c_int32), V]
+    lib.cssar_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]
     for s in SYMBOLS:
         if s != "cssar_error_string":
             getattr(lib, s).restype = I
@@ -181,13 +184,14 @@ class Plan:
         return out
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
-                    log=False, stream=None):
+                    log=False, profile_stages=False, stream=None):
         """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X."""
         if X is None:
             X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
         prm = ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
-                         int(k), float(lam), float(mu), int(iters), 0)
+                         int(k), float(lam), float(mu), int(iters),
+                         CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0)
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
                                         logbuf if log else None, _stream(stream))
@@ -197,6 +201,24 @@ class Plan:
                        for e in list(logbuf)[:iters]]
             return X, entries
         return X
+
+    def stage_times(self):
+        """Per-step device milliseconds (summed) of the last profile_stages run, and its iterations."""
+        ms = (ctypes.c_double * 6)()
+        it = ctypes.c_int32()
+        _check(self.lib.cssar_stage_times(self.h, ms, ctypes.byref(it)), "cssar_stage_times")
+        return dict(zip(STAGES, list(ms))), it.value
+
+    def solve_host(self, Y_host, mask_bits_host, out_host=None, stream=None, **ita_kw):
+        """End-to-end user call: host (pinned) Y and mask -> device -> ITA -> host X."""
+        Y = Y_host.to("cuda", non_blocking=True)
+        mb = None if mask_bits_host is None else mask_bits_host.to("cuda", non_blocking=True)
+        X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
+        self.ita_iterate(Y, mb, X=X, stream=stream, **ita_kw)
+        if out_host is None:
+            out_host = torch.empty(self.shape, dtype=torch.complex64, pin_memory=True)
+        out_host.copy_(X, non_blocking=True)
+        return out_host
 
     # ---- test hooks
     def debug_range_sweep(self, U, gbody, stream=None):
