@@ -8,13 +8,15 @@ namespace cssar {
 // ------------------------------------------------------------------ azimuth sweeps
 template <int LOGN>
 struct AzCfg {
-  // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each)
-  static constexpr int C = LOGN == 12 ? 2 : LOGN == 13 ? 8 : LOGN == 14 ? 8 : LOGN == 15 ? 16 : 1;
-  static constexpr int W = LOGN <= 9 ? 16 : LOGN == 10 ? 8 : LOGN == 13 ? 8 : 4;
+  // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
+  // 4096-8192 complex64 per CTA (32-64 KB SMEM), E = 16 elements per thread
+  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
+  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : 4;
   static constexpr int LOGM = LOGN - ilog2c(C);
   static constexpr int M = 1 << LOGM;
-  static constexpr int E = plan_E(LOGM);
+  static constexpr int E = 16;
   static constexpr int T = M * W / E;
+  static constexpr int MINB = T <= 256 ? 3 : 2;
   static constexpr size_t SMEM_FFT = sizeof(float2) * M * W;
   static constexpr int CAND_SMEM = 1024;
   static constexpr size_t SMEM_TAIL = SMEM_FFT + sizeof(uint32_t) * (HIST_BINS + CAND_SMEM + 4);
@@ -23,10 +25,17 @@ struct AzCfg {
 struct TailCtx {
   uint32_t* shist;
   uint32_t* scand;
-  uint32_t* scount;      // [0] = candidates in SMEM, [1] = fixed-lambda survivors, [2] = overflow
+  uint32_t* scount;      // [0] = candidates in SMEM, [1] = fixed-lambda survivors
   int floor_bin, cand_lo, cand_hi;
   uint32_t s2bits, s2fixed;
   float sigma;
+};
+
+// auxiliary per-element inputs, fetched for a whole group before any arithmetic so the
+// loads are in flight together (long-scoreboard latency overlaps)
+struct Aux {
+  float2 v;        // Y (RESID) or b_{i-1} (TAIL)
+  uint32_t m;      // mask bit
 };
 
 template <int MODE>
@@ -42,26 +51,34 @@ struct AzOps {
     return v;
   }
 
-  // RESID mid: g = G(X) sample; r = Theta o (Y - g)
-  CSSAR_DEV static float2 mid(const AzArgs& a, int row, int col, size_t idx, float2 x, float& acc) {
-    const float2 g = x * a.scale;
-    float2 r = make_float2(0.f, 0.f);
-    if (mask_bit(a.mask, a.mask_words, row, col)) {
-      const float2 y = __ldg(a.Y + idx);
-      r = y - g;
+  CSSAR_DEV static Aux fetch(const AzArgs& a, int row, int col, size_t idx) {
+    Aux x{make_float2(0.f, 0.f), 1u};
+    if constexpr (MODE == AZ_RESID) {
+      x.m = mask_bit(a.mask, a.mask_words, row, col);
+      x.v = __ldg(a.Y + idx);
+    } else if constexpr (MODE == AZ_INV_MASK) {
+      x.m = mask_bit(a.mask, a.mask_words, row, col);
+    } else if constexpr (MODE == AZ_TAIL) {
+      x.v = a.b[idx];
     }
+    return x;
+  }
+
+  // RESID mid: g = G(X) sample; r = Theta o (Y - g)
+  CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc) {
+    const float2 g = x * a.scale;
+    const float2 r = ax.m ? (ax.v - g) : make_float2(0.f, 0.f);
     acc = fmaf(r.x, r.x, fmaf(r.y, r.y, acc));
     return r;
   }
 
-  CSSAR_DEV static void epi(const AzArgs& a, int row, int col, size_t idx, float2 x, TailCtx& tc) {
+  CSSAR_DEV static void epi(const AzArgs& a, size_t idx, float2 x, const Aux& ax, TailCtx& tc) {
     float2 v = x * a.scale;
     if constexpr (MODE == AZ_INV_MASK) {
-      if (!mask_bit(a.mask, a.mask_words, row, col)) v = make_float2(0.f, 0.f);
+      if (!ax.m) v = make_float2(0.f, 0.f);
     }
     if constexpr (MODE == AZ_TAIL) {
-      const float2 bp = a.b[idx];
-      const float2 xk = threshold(bp, tc.s2bits, tc.sigma, a.thr);     // X_i recomputed
+      const float2 xk = threshold(ax.v, tc.s2bits, tc.sigma, a.thr);     // X_i recomputed
       const float2 bn = make_float2(fmaf(a.mu, v.x, xk.x), fmaf(a.mu, v.y, xk.y));
       a.b[idx] = bn;
       const uint32_t u = mag2_bits(bn);
@@ -70,7 +87,7 @@ struct AzOps {
         if (bin >= tc.floor_bin) atomicAdd(&tc.shist[bin], 1u);
         if (bin >= tc.cand_lo && bin <= tc.cand_hi) {
           const uint32_t pos = atomicAdd(&tc.scount[0], 1u);
-          if (pos < (uint32_t)AzCfg<7>::CAND_SMEM) {
+          if (pos < 1024u) {
             tc.scand[pos] = u;
           } else {
             const uint32_t g = atomicAdd(&a.st->cand_count, 1u);
@@ -89,11 +106,11 @@ struct AzOps {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
+__global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<LOGN>::MINB) az_kernel(const AzArgs a) {
   using Cf = AzCfg<LOGN>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
-  using En = Engine<Cf::LOGM, W, T, true>;
+  using En = Engine<Cf::LOGM, W, T, true, E>;
   using Ops = AzOps<MODE>;
   constexpr int R0 = 1 << En::template lr<false>(0);
   constexpr int RL = 1 << En::template lr<false>(En::P - 1);
@@ -135,11 +152,14 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
   if constexpr (C == 1) {
     if constexpr (MODE == AZ_RESID) {
       auto mid = [&](int w, int j, float2* x) {
+        Aux ax[RL];
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = j + r * (M / RL);
-          x[r] = Ops::mid(a, row, col0 + w, (size_t)row * n_rg + col0 + w, x[r], racc);
+          ax[r] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
         }
+#pragma unroll
+        for (int r = 0; r < RL; ++r) x[r] = Ops::mid(a, x[r], ax[r], racc);
       };
       auto st = [&](int w, int j, float2* x) {
 #pragma unroll
@@ -151,10 +171,16 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
       En::template conv<+1>(s, ld, mid, st);
     } else {
       auto st = [&](int w, int j, float2* x) {
+        Aux ax[RL];
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = j + r * (M / RL);
-          Ops::epi(a, row, col0 + w, (size_t)row * n_rg + col0 + w, x[r], tc);
+          ax[r] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+        }
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int row = j + r * (M / RL);
+          Ops::epi(a, (size_t)row * n_rg + col0 + w, x[r], ax[r], tc);
         }
       };
       En::template run<Ops::DIR>(s, ld, st);
@@ -166,7 +192,8 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
     En::store_natural(s, v);
     cluster.sync();
     // gather: this rank owns local output indices k in [rank M/C, (rank+1) M/C)
-    constexpr int PT = E / C;                       // (k, w) pairs per thread
+    constexpr int PT = E / C > 0 ? E / C : 1;       // (k, w) pairs per thread
+    static_assert((M / C) * W == PT * T, "cluster gather shape");
     float2 z[PT][C];
 #pragma unroll
     for (int p = 0; p < PT; ++p) {
@@ -177,6 +204,25 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
         const float2* rs = cluster.map_shared_rank(s, c);
         z[p][c] = rs[k * W + w];
       }
+    }
+    // auxiliary inputs of the elements this thread finalises (rows k + M q)
+    Aux ax[PT][C];
+    if constexpr (MODE == AZ_RESID || MODE == AZ_TAIL || MODE == AZ_INV_MASK) {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const int pr = p * T + t;
+        const int w = pr % W, k = rank * (M / C) + pr / W;
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          const int row = k + M * q;
+          ax[p][q] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PT; ++p) {
+      const int pr = p * T + t;
+      const int k = rank * (M / C) + pr / W;
 #pragma unroll
       for (int c = 1; c < C; ++c)
         z[p][c] = cmul(z[p][c], expi_frac<Ops::DIR>((uint32_t)(c * k) & (N - 1), (uint32_t)N));
@@ -186,12 +232,9 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
         const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
+        const int k = rank * (M / C) + pr / W;
 #pragma unroll
-        for (int q = 0; q < C; ++q) {
-          const int row = k + M * q;
-          z[p][q] = Ops::mid(a, row, col0 + w, (size_t)row * n_rg + col0 + w, z[p][q], racc);
-        }
+        for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
         // forward DIF first stage: y_q = (sum_q' x_q' w_C^{q q'}) w_N^{q k}
         dft<C, -1>(z[p]);
 #pragma unroll
@@ -227,7 +270,7 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T) az_kernel(const AzArgs a) {
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
-          Ops::epi(a, row, col0 + w, (size_t)row * n_rg + col0 + w, z[p][q], tc);
+          Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
         }
       }
       cluster.sync();                                  // keep SMEM alive for remote readers

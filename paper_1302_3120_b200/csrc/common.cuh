@@ -90,22 +90,44 @@ CSSAR_DEV float2 expi_frac(uint32_t num, uint32_t den) {
   return make_float2(c, DIR > 0 ? s : -s);
 }
 
-// Twiddles w^r, r = 0..R-1, with w = exp(DIR 2 pi i k / L): exact anchors w^(2^a) from
-// sincospif on the reduced integer argument, other powers as products of anchors
-// (<= log2(R)-1 roundings each).
+// x[r] *= w^r, r = 1..R-1, w = exp(DIR 2 pi i k / L): exact anchors w^(2^a) from sincospif
+// on the reduced integer argument; w^r = w^(r - lowbit(r)) * anchor(lowbit(r)), i.e. at
+// most log2(R) - 1 roundings per power.
 template <int R, int DIR>
-CSSAR_DEV void twiddle_powers(uint32_t k, uint32_t L, float2 (&w)[R]) {
+CSSAR_DEV void apply_twiddles(float2* x, uint32_t k, uint32_t L) {
   constexpr int LR = Log2<R>::v;
   float2 anc[LR > 0 ? LR : 1];
 #pragma unroll
   for (int a = 0; a < LR; ++a) anc[a] = expi_frac<DIR>((k << a) & (L - 1), L);
+  float2 w[R];
   w[0] = make_float2(1.f, 0.f);
 #pragma unroll
   for (int r = 1; r < R; ++r) {
-    const int low = r & (-r);           // lowest set bit
+    const int low = r & (-r);
     const int a = ilog2c(low);
-    if (r == low) w[r] = anc[a];
-    else w[r] = cmul(w[r - low], anc[a]);
+    w[r] = (r == low) ? anc[a] : cmul(w[r - low], anc[a]);
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r) x[r] = cmul(x[r], w[r]);
+}
+
+// exp(2 pi i t / 2^24) for a 24-bit integer t from a 256-entry SMEM table of exp(2 pi i h/256)
+// (top 8 bits) times a short polynomial for the low 16 bits (|theta| < 2 pi/256:
+// cos error theta^4/24 < 1.6e-8, sin error theta^5/120 < 1e-10).
+CSSAR_DEV float2 expi24(const float2* tab256, uint32_t t) {
+  const float2 h = tab256[t >> 16];
+  const float th = (float)(t & 0xFFFFu) * 3.7450702829239464e-07f;   // 2 pi / 2^24
+  const float t2 = th * th;
+  const float c = fmaf(-0.5f, t2, 1.0f);
+  const float s = th * fmaf(-0.16666667f, t2, 1.0f);
+  return make_float2(fmaf(h.x, c, -h.y * s), fmaf(h.x, s, h.y * c));
+}
+
+CSSAR_DEV void init_expi_table(float2* tab256, int t, int nthreads) {
+  for (int i = t; i < 256; i += nthreads) {
+    float s, c;
+    sincospif((float)i * (1.0f / 128.0f), &s, &c);
+    tab256[i] = make_float2(c, s);
   }
 }
 
@@ -122,13 +144,18 @@ CSSAR_DEV uint64_t quad_eval(const Quad& q, int32_t u) {
   return q.c2 * u2 + q.c1 * uu + q.c0;
 }
 
-// exp(+-2 pi i P / 2^64)
+// exp(+-2 pi i P / 2^64): top 24 bits rounded to nearest, table + polynomial
 template <bool CONJ>
-CSSAR_DEV float2 phase_from_fixed(uint64_t P) {
-  uint32_t t = (uint32_t)((P + (1ull << 39)) >> 40) & 0xFFFFFFu;   // 24-bit, rounded
+CSSAR_DEV float2 phase_from_fixed(const float2* tab256, uint64_t P) {
+  const uint32_t t = (uint32_t)((P + (1ull << 39)) >> 40) & 0xFFFFFFu;
+#if defined(CSSAR_PHASE_SINCOSPIF)
   float s, c;
-  sincospif((float)t * (1.0f / 8388608.0f), &s, &c);              // pi * t / 2^23 = 2 pi t / 2^24
-  return make_float2(c, CONJ ? -s : s);
+  sincospif((float)t * (1.0f / 8388608.0f), &s, &c);
+  const float2 e = make_float2(c, s);
+#else
+  const float2 e = expi24(tab256, t);
+#endif
+  return make_float2(e.x, CONJ ? -e.y : e.y);
 }
 
 }  // namespace cssar

@@ -48,13 +48,13 @@ CSSAR_DEV uint32_t mask_bit(const uint32_t* mask, int words, int row, int col) {
 
 // x[r] *= exp(+-2 pi i P(u0 + r S)), r < R, by exact u64 second differences
 template <int R, int S, bool CONJ>
-CSSAR_DEV void phase_apply(const Quad& q, int u0, float2* x) {
+CSSAR_DEV void phase_apply(const float2* tab, const Quad& q, int u0, float2* x) {
   uint64_t P = quad_eval(q, u0);
   uint64_t d1 = q.c2 * (uint64_t)((int64_t)2 * u0 * S + (int64_t)S * S) + q.c1 * (uint64_t)S;
   const uint64_t d2 = q.c2 * (uint64_t)(2ll * S * S);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    x[r] = cmul(x[r], phase_from_fixed<CONJ>(P));
+    x[r] = cmul(x[r], phase_from_fixed<CONJ>(tab, P));
     P += d1;
     d1 += d2;
   }

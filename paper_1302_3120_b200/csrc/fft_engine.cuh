@@ -22,11 +22,22 @@
 
 namespace cssar {
 
-// ----- radix plans: log2 of the radix of each pass, and elements per thread ----------------
-CSSAR_DEV constexpr int plan_passes(int logn) { return logn <= 8 ? 2 : logn <= 10 ? 2 : 3; }
-CSSAR_DEV constexpr int plan_lr(int logn, int p) {
-  // 7:[16,8] 8:[16,16] 9:[16,32] 10:[32,32] 11:[16,8,16] 12:[16,16,16] 13:[16,32,16]
-  // 14:[32,16,32] 15:[32,32,32]
+// ----- radix plans: log2 of the radix of each pass for a length 2^logn with E elements per
+// thread (every radix <= E).  E = 32: 7:[16,8] 8:[16,16] 9:[16,32] 10:[32,32] 11:[16,8,16]
+// 12:[16,16,16] 13:[16,32,16] 14:[32,16,32] 15:[32,32,32].  E = 16: 7:[16,8] 8:[16,16]
+// 9:[8,8,8] 10:[16,8,8] 11:[16,8,16] 12:[16,16,16].
+CSSAR_DEV constexpr int plan_passes(int logn, int E) {
+  return E == 16 ? (logn <= 8 ? 2 : 3) : (logn <= 10 ? 2 : 3);
+}
+CSSAR_DEV constexpr int plan_lr(int logn, int E, int p) {
+  if (E == 16) {
+    return logn == 7 ? (p == 0 ? 4 : 3)
+         : logn == 8 ? 4
+         : logn == 9 ? 3
+         : logn == 10 ? (p == 0 ? 4 : 3)
+         : logn == 11 ? (p == 1 ? 3 : 4)
+         : 4;
+  }
   return logn == 7 ? (p == 0 ? 4 : 3)
        : logn == 8 ? 4
        : logn == 9 ? (p == 0 ? 4 : 5)
@@ -37,21 +48,22 @@ CSSAR_DEV constexpr int plan_lr(int logn, int p) {
        : logn == 14 ? (p == 1 ? 4 : 5)
        : 5;
 }
-CSSAR_DEV constexpr int plan_E(int logn) {
-  return (logn == 9 || logn == 10 || logn == 13 || logn == 14 || logn == 15) ? 32 : 16;
+CSSAR_DEV constexpr bool plan_ok(int logn, int E) {
+  return (E == 32 && logn >= 7 && logn <= 15) || (E == 16 && logn >= 7 && logn <= 12);
 }
 
-template <int LOGN, int B, int T, bool BMINOR>
+template <int LOGN, int B, int T, bool BMINOR, int E_ = 32>
 struct Engine {
   static constexpr int N = 1 << LOGN;
-  static constexpr int P = plan_passes(LOGN);
-  static constexpr int E = plan_E(LOGN);
+  static constexpr int E = E_;
+  static_assert(plan_ok(LOGN, E), "no radix plan for this (N, E)");
+  static constexpr int P = plan_passes(LOGN, E);
   static_assert(N * B == T * E, "CTA shape must give E elements per thread");
   static constexpr int G = BMINOR ? (B >= 16 ? 1 : 16 / B) : 16;
 
   // radix / NS of pass p; REV = passes in reverse order (the inverse half of fft_conv)
   template <bool REV>
-  static CSSAR_DEV constexpr int lr(int p) { return plan_lr(LOGN, REV ? P - 1 - p : p); }
+  static CSSAR_DEV constexpr int lr(int p) { return plan_lr(LOGN, E, REV ? P - 1 - p : p); }
   template <bool REV>
   static CSSAR_DEV constexpr int lns(int p) {
     int s = 0;
@@ -88,12 +100,7 @@ struct Engine {
       float2 x[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = v[m * R + r];
-      if constexpr (NS > 1) {
-        float2 w[R];
-        twiddle_powers<R, DIR>((uint32_t)(j & (NS - 1)), (uint32_t)(NS * R), w);
-#pragma unroll
-        for (int r = 1; r < R; ++r) x[r] = cmul(x[r], w[r]);
-      }
+      if constexpr (NS > 1) apply_twiddles<R, DIR>(x, (uint32_t)(j & (NS - 1)), (uint32_t)(NS * R));
       dft<R, DIR>(x);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[m * R + r] = x[r];

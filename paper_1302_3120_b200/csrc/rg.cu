@@ -7,24 +7,31 @@ namespace cssar {
 template <int LOGN>
 struct RgCfg {
   static constexpr int N = 1 << LOGN;
-  static constexpr int E = plan_E(LOGN);
+  static constexpr int E = 32;
   static constexpr int T = LOGN >= 14 ? 512 : 256;
   static constexpr int B = (T * E) / N > 0 ? (T * E) / N : 1;
-  static constexpr size_t SMEM = sizeof(float2) * N * B;
+#ifndef CSSAR_RG_MINB
+#define CSSAR_RG_MINB 2
+#endif
+  static constexpr int MINB = LOGN >= 14 ? 1 : CSSAR_RG_MINB;   // resident CTAs per SM (register cap)
+  static constexpr size_t SMEM = sizeof(float2) * (N * B + 256);
 };
 
 // GBODY: Phi3* -> F -> Phi2* -> F^-1 -> Phi1*  (inverse of the focusing steps)
 // else : Phi1  -> F -> Phi2  -> F^-1 -> Phi3   (CSA focusing body)
 template <int LOGN, bool GBODY>
-__global__ void __launch_bounds__(RgCfg<LOGN>::T) rg_sweep_kernel(const RgArgs a) {
+__global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_kernel(const RgArgs a) {
   using C = RgCfg<LOGN>;
-  using En = Engine<LOGN, C::B, C::T, false>;
+  using En = Engine<LOGN, C::B, C::T, false, C::E>;
   constexpr int N = C::N;
   constexpr int R0 = 1 << En::template lr<false>(0);
   constexpr int RL = 1 << En::template lr<false>(En::P - 1);
   extern __shared__ float4 smem4[];
   float2* s = reinterpret_cast<float2*>(smem4);
   const int row0 = blockIdx.x * C::B;
+  float2* tab = s + N * C::B;                 // exp(2 pi i h / 256) for the phase generator
+  init_expi_table(tab, threadIdx.x, C::T);
+  __syncthreads();
   float2* __restrict__ data = a.data;
 
   auto ld = [&](int b, int j, float2* x) {
@@ -32,17 +39,17 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T) rg_sweep_kernel(const RgArgs a
 #pragma unroll
     for (int r = 0; r < R0; ++r) x[r] = src[j + r * (N / R0)];
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
-    phase_apply<R0, N / R0, GBODY>(q, j - N / 2, x);
+    phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
   };
   auto mid = [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[1];
     // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
-    phase_apply<RL / 2, N / RL, GBODY>(q, j, x);
-    phase_apply<RL / 2, N / RL, GBODY>(q, j - N / 2, x + RL / 2);
+    phase_apply<RL / 2, N / RL, GBODY>(tab, q, j, x);
+    phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
   };
   auto st = [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
-    phase_apply<R0, N / R0, GBODY>(q, j - N / 2, x);
+    phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     float2* dst = data + (size_t)(row0 + b) * N;
 #pragma unroll
     for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r] * a.scale;

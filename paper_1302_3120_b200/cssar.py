@@ -57,11 +57,13 @@ class IterLogC(ctypes.Structure):
 _lib = None
 
 
-def load_library(path=LIB_PATH):
-    """Load libcssar.so (raises if it was not built: there is no fallback)."""
+def load_library(path=None):
+    """Load libcssar.so (raises if it was not built: there is no fallback).  CSSAR_LIB may
+    point at a tuning variant of the same library (tools/variants.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("CSSAR_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise FileNotFoundError(f"{path} not built; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)
