@@ -9,17 +9,31 @@ namespace cssar {
 template <int LOGN>
 struct AzCfg {
   // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
-  // 4096-8192 complex64 per CTA (32-64 KB SMEM), E = 16 elements per thread
+  // 4096-8192 complex64 per CTA (32-64 KB SMEM), E elements per thread
   static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
   static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : 4;
+  static constexpr int E = 16;
+};
+#if defined(CSSAR_AZ13_C)
+template <>
+struct AzCfg<13> {
+  static constexpr int C = CSSAR_AZ13_C, W = CSSAR_AZ13_W, E = CSSAR_AZ13_E;
+};
+#endif
+
+template <int LOGN>
+struct AzShape {
+  using P = AzCfg<LOGN>;
+  static constexpr int C = P::C, W = P::W, E = P::E;
   static constexpr int LOGM = LOGN - ilog2c(C);
   static constexpr int M = 1 << LOGM;
-  static constexpr int E = 16;
   static constexpr int T = M * W / E;
-  static constexpr int MINB = T <= 256 ? 3 : 2;
+  static constexpr int MINB = T <= 128 ? 4 : T <= 256 ? (E == 32 ? 2 : 3) : (E == 32 ? 1 : 2);
+  static constexpr int NBUF = C > 1 ? 2 : 1;               // RESID double-buffers the scatter
   static constexpr size_t SMEM_FFT = sizeof(float2) * M * W;
   static constexpr int CAND_SMEM = 1024;
   static constexpr size_t SMEM_TAIL = SMEM_FFT + sizeof(uint32_t) * (HIST_BINS + CAND_SMEM + 4);
+  static constexpr size_t SMEM_RESID = SMEM_FFT * NBUF;
 };
 
 struct TailCtx {
@@ -106,8 +120,9 @@ struct AzOps {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<LOGN>::MINB) az_kernel(const AzArgs a) {
-  using Cf = AzCfg<LOGN>;
+__global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape<LOGN>::MINB > 2) ? 2 : AzShape<LOGN>::MINB)
+    az_kernel(const AzArgs a) {
+  using Cf = AzShape<LOGN>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
   using En = Engine<Cf::LOGM, W, T, true, E>;
@@ -205,6 +220,7 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<L
         z[p][c] = rs[k * W + w];
       }
     }
+    if constexpr (MODE != AZ_RESID) cluster.barrier_arrive();    // done reading remote SMEM
     // auxiliary inputs of the elements this thread finalises (rows k + M q)
     Aux ax[PT][C];
     if constexpr (MODE == AZ_RESID || MODE == AZ_TAIL || MODE == AZ_INV_MASK) {
@@ -223,9 +239,7 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<L
     for (int p = 0; p < PT; ++p) {
       const int pr = p * T + t;
       const int k = rank * (M / C) + pr / W;
-#pragma unroll
-      for (int c = 1; c < C; ++c)
-        z[p][c] = cmul(z[p][c], expi_frac<Ops::DIR>((uint32_t)(c * k) & (N - 1), (uint32_t)N));
+      apply_twiddles<C, Ops::DIR>(z[p], (uint32_t)k, (uint32_t)N);   // w_N^{c k}
       dft<C, Ops::DIR>(z[p]);                         // z[q] = X[k + M q]
     }
     if constexpr (MODE == AZ_RESID) {
@@ -237,22 +251,23 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<L
         for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
         // forward DIF first stage: y_q = (sum_q' x_q' w_C^{q q'}) w_N^{q k}
         dft<C, -1>(z[p]);
-#pragma unroll
-        for (int q = 1; q < C; ++q)
-          z[p][q] = cmul(z[p][q], expi_frac<-1>((uint32_t)(q * k) & (N - 1), (uint32_t)N));
+        apply_twiddles<C, -1>(z[p], (uint32_t)k, (uint32_t)N);       // w_N^{-q k}
       }
-      cluster.sync();                                  // all gathers done before overwriting
+      // scatter into the second SMEM buffer of CTA q (no barrier needed against the gathers,
+      // which read the first buffer)
+      float2* s2 = s + M * W;
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
         const int pr = p * T + t;
         const int w = pr % W, k = rank * (M / C) + pr / W;
 #pragma unroll
         for (int q = 0; q < C; ++q) {
-          float2* rs = cluster.map_shared_rank(s, q);
+          float2* rs = cluster.map_shared_rank(s2, q);
           rs[k * W + w] = z[p][q];
         }
       }
       cluster.sync();
+      s = s2;
       // local forward FFT of y_rank: X[C m + rank] -> row rank + C m
       auto st = [&](int w, int j, float2* x) {
 #pragma unroll
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<L
           Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
         }
       }
-      cluster.sync();                                  // keep SMEM alive for remote readers
+      cluster.barrier_wait();                          // keep SMEM alive for remote readers
     }
   }
 
@@ -315,9 +330,9 @@ __global__ void __launch_bounds__(AzCfg<LOGN>::T, MODE == AZ_RESID ? 2 : AzCfg<L
 
 template <int LOGN, int MODE>
 static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
-  using Cf = AzCfg<LOGN>;
+  using Cf = AzShape<LOGN>;
   auto k = az_kernel<LOGN, MODE>;
-  const size_t smem = (MODE == AZ_TAIL) ? Cf::SMEM_TAIL : Cf::SMEM_FFT;
+  const size_t smem = (MODE == AZ_TAIL) ? Cf::SMEM_TAIL : (MODE == AZ_RESID) ? Cf::SMEM_RESID : Cf::SMEM_FFT;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (Cf::C > 8) {
