@@ -36,6 +36,8 @@ struct cssar_plan_s {
   long long n = 0;
   int sm_count = 148;
   RowCoef* d_coef = nullptr;
+  float2* d_rg_tab = nullptr;     // phase exp table + range-engine twiddles
+  float2* d_az_tab = nullptr;     // azimuth-engine twiddles
   SelState* d_st = nullptr;
   uint32_t* d_hist = nullptr;
   uint32_t* d_hist_full = nullptr;
@@ -140,13 +142,14 @@ int validate_params(const cssar_sar_params& p) {
 
 int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yout, cudaStream_t s) {
   AzArgs a{};
+  a.tw = pl->d_az_tab;
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
   a.in = (const float2*)X;
   a.out = (float2*)Yout;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_PLAIN, a.n_rg, a, s));
-  RgArgs r{(float2*)Yout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg)};
+  RgArgs r{(float2*)Yout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Yout;
   a.mask = mask;
@@ -156,6 +159,7 @@ int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yo
 
 int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xout, cudaStream_t s) {
   AzArgs a{};
+  a.tw = pl->d_az_tab;
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
@@ -163,7 +167,7 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
   a.out = (float2*)Xout;
   a.mask = mask;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_MASK, a.n_rg, a, s));
-  RgArgs r{(float2*)Xout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg)};
+  RgArgs r{(float2*)Xout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Xout;
   a.mask = nullptr;
@@ -176,6 +180,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
                       cudaStream_t s, bool prof = false) {
 #define MARK(i) do { if (prof) CUDA_TRY(cudaEventRecord(pl->ev[i], s)); } while (0)
   AzArgs a{};
+  a.tw = pl->d_az_tab;
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
@@ -189,7 +194,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.Y = (const float2*)Y;
   a.mask = mask;
   float2* b = (float2*)X;
-  RgArgs r{pl->U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg)};
+  RgArgs r{pl->U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
   MARK(0);
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
   a.in = b;
@@ -270,7 +275,12 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
       cudaMalloc(&pl->d_hist, sizeof(uint32_t) * HIST_BINS) != cudaSuccess ||
       cudaMalloc(&pl->d_hist_full, sizeof(uint32_t) * HIST_BINS) != cudaSuccess ||
       cudaMalloc(&pl->d_log, sizeof(IterLogDev) * kLogCap) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&pl->d_rg_tab, sizeof(float2) * rg_table_count(pl->log_nrg)) != cudaSuccess ||
+      cudaMalloc(&pl->d_az_tab, sizeof(float2) * (az_table_count(pl->log_naz) + 2)) != cudaSuccess ||
+      rg_table_fill(pl->log_nrg, pl->d_rg_tab, pl->cap_stream) != cudaSuccess ||
+      az_table_fill(pl->log_naz, pl->d_az_tab, pl->cap_stream) != cudaSuccess ||
+      cudaStreamSynchronize(pl->cap_stream) != cudaSuccess) {
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
@@ -290,6 +300,8 @@ int cssar_plan_destroy(cssar_plan pl) {
   for (int i = 0; i < 7; ++i)
     if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
   cudaFree(pl->d_coef);
+  cudaFree(pl->d_rg_tab);
+  cudaFree(pl->d_az_tab);
   cudaFree(pl->d_st);
   cudaFree(pl->d_hist);
   cudaFree(pl->d_hist_full);
@@ -418,7 +430,7 @@ int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, i
 int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
-  RgArgs r{(float2*)U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg)};
+  RgArgs r{(float2*)U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody != 0, (int)pl->p.n_az, r, (cudaStream_t)stream));
   return CSSAR_OK;
 }
@@ -427,6 +439,7 @@ int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* 
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(in) || !aligned16(out)) return CSSAR_ERR_ALIGNMENT;
   AzArgs a{};
+  a.tw = pl->d_az_tab;
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));

@@ -30,10 +30,12 @@ struct AzShape {
   static constexpr int T = M * W / E;
   static constexpr int MINB = T <= 128 ? 4 : T <= 256 ? (E == 32 ? 2 : 3) : (E == 32 ? 1 : 2);
   static constexpr int NBUF = C > 1 ? 2 : 1;               // RESID double-buffers the scatter
-  static constexpr size_t SMEM_FFT = sizeof(float2) * M * W;
+  using En = Engine<LOGM, W, T, true, E>;
+  static constexpr int TW = En::TW_TOTAL;
+  static constexpr size_t SMEM_FFT = sizeof(float2) * (M * W + TW);
   static constexpr int CAND_SMEM = 1024;
   static constexpr size_t SMEM_TAIL = SMEM_FFT + sizeof(uint32_t) * (HIST_BINS + CAND_SMEM + 4);
-  static constexpr size_t SMEM_RESID = SMEM_FFT * NBUF;
+  static constexpr size_t SMEM_RESID = SMEM_FFT + sizeof(float2) * M * W * (NBUF - 1);
 };
 
 struct TailCtx {
@@ -125,13 +127,16 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
   using Cf = AzShape<LOGN>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
-  using En = Engine<Cf::LOGM, W, T, true, E>;
+  using En = typename Cf::En;
   using Ops = AzOps<MODE>;
   constexpr int R0 = 1 << En::template lr<false>(0);
   constexpr int RL = 1 << En::template lr<false>(En::P - 1);
 
   extern __shared__ float4 smem4[];
-  float2* s = reinterpret_cast<float2*>(smem4);
+  float2* tw = reinterpret_cast<float2*>(smem4);      // inter-pass twiddle tables
+  float2* s = tw + Cf::TW;                             // panel data
+  copy_table(tw, a.tw, Cf::TW, threadIdx.x, Cf::T);
+  __syncthreads();
   int rank = 0;
   if constexpr (C > 1) rank = (int)cg::this_cluster().block_rank();
   const int col0 = (blockIdx.x / C) * W;
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
           a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
         }
       };
-      En::template conv<+1>(s, ld, mid, st);
+      En::template conv<+1>(s, ld, mid, st, tw);
     } else {
       auto st = [&](int w, int j, float2* x) {
         Aux ax[RL];
@@ -198,12 +203,12 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
           Ops::epi(a, (size_t)row * n_rg + col0 + w, x[r], ax[r], tc);
         }
       };
-      En::template run<Ops::DIR>(s, ld, st);
+      En::template run<Ops::DIR>(s, ld, st, tw);
     }
   } else {
     auto cluster = cg::this_cluster();
     float2 v[E];
-    En::template run_keep<Ops::DIR>(s, v, ld);
+    En::template run_keep<Ops::DIR>(s, v, ld, tw);
     En::store_natural(s, v);
     cluster.sync();
     // gather: this rank owns local output indices k in [rank M/C, (rank+1) M/C)
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
           a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
         }
       };
-      En::template run_from_smem<-1>(s, st);
+      En::template run_from_smem<-1>(s, st, tw);
     } else {
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
@@ -353,6 +358,20 @@ static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, k, a);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <int LOGN>
+__global__ void az_table_kernel(float2* dst) {
+  AzShape<LOGN>::En::build_tw(dst, threadIdx.x, blockDim.x);
+}
+
+template <int LOGN>
+size_t az_table_count_t() { return (size_t)AzShape<LOGN>::TW; }
+
+template <int LOGN>
+cudaError_t az_table_fill_t(float2* dst, cudaStream_t s) {
+  az_table_kernel<LOGN><<<1, 256, 0, s>>>(dst);
   return cudaGetLastError();
 }
 

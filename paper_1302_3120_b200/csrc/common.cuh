@@ -123,6 +123,13 @@ CSSAR_DEV float2 expi24(const float2* tab256, uint32_t t) {
   return make_float2(fmaf(h.x, c, -h.y * s), fmaf(h.x, s, h.y * c));
 }
 
+// cooperative copy of n (even) float2 from global to SMEM with 16-byte accesses
+CSSAR_DEV void copy_table(float2* dst, const float2* src, int n, int t, int nthreads) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int i = t; i < n / 2; i += nthreads) d4[i] = __ldg(s4 + i);
+}
+
 CSSAR_DEV void init_expi_table(float2* tab256, int t, int nthreads) {
   for (int i = t; i < 256; i += nthreads) {
     float s, c;

@@ -71,6 +71,74 @@ struct Engine {
     return s;
   }
 
+  // ---- inter-pass twiddle tables (SMEM, forward sign; conjugated on use for DIR = +1).
+  // Pass (NS, R), L = NS R: single level T[r NS + k] = w_L^{r k} when L <= 1024, else two
+  // levels with k = 64 kh + kl: lo[r 64 + kl] = w_L^{r kl}, hi[r (NS/64) + kh] = w_L^{64 r kh}.
+  static CSSAR_DEV constexpr int tw_size_of(int lns, int lr) {
+    return lns == 0 ? 0 : (lns + lr <= 10) ? (1 << (lns + lr)) : ((1 << lr) * 64 + (1 << lr) * (1 << (lns - 6)));
+  }
+  // forward pass with the same (NS, R) as reverse pass p, or 0 if none
+  static CSSAR_DEV constexpr int tw_same_fwd(int p) {
+    for (int q = 1; q < P; ++q)
+      if (lns<false>(q) == lns<true>(p) && lr<false>(q) == lr<true>(p)) return q;
+    return 0;
+  }
+  template <bool REV>
+  static CSSAR_DEV constexpr int tw_off(int p) {
+    if (REV && tw_same_fwd(p)) return tw_off<false>(tw_same_fwd(p));
+    int o = 0;
+    if (REV) {
+      for (int q = 1; q < P; ++q) o += tw_size_of(lns<false>(q), lr<false>(q));
+      for (int q = 1; q < p; ++q)
+        if (!tw_same_fwd(q)) o += tw_size_of(lns<true>(q), lr<true>(q));
+    } else {
+      for (int q = 1; q < p; ++q) o += tw_size_of(lns<false>(q), lr<false>(q));
+    }
+    return o;
+  }
+  static CSSAR_DEV constexpr int tw_total() {
+    int o = 0;
+    for (int q = 1; q < P; ++q) o += tw_size_of(lns<false>(q), lr<false>(q));
+    for (int q = 1; q < P; ++q)
+      if (!tw_same_fwd(q)) o += tw_size_of(lns<true>(q), lr<true>(q));
+    return o;
+  }
+  static constexpr int TW_TOTAL = tw_total();
+
+  // fill the twiddle tables (one entry per thread-iteration; exact sincospif arguments)
+  static CSSAR_DEV void build_tw(float2* tw, int t, int nthreads) {
+    build_tw_rev<false, 1>(tw, t, nthreads);
+    build_tw_rev<true, 1>(tw, t, nthreads);
+  }
+  template <bool REV, int p>
+  static CSSAR_DEV void build_tw_rev(float2* tw, int t, int nthreads) {
+    if constexpr (p < P) {
+      if constexpr (REV && tw_same_fwd(p) != 0) {
+        build_tw_rev<REV, p + 1>(tw, t, nthreads);
+        return;
+      }
+      constexpr int LR = lr<REV>(p), LNS = lns<REV>(p);
+      constexpr int R = 1 << LR, NS = 1 << LNS, L = NS * R;
+      float2* base = tw + tw_off<REV>(p);
+      if constexpr (L <= 1024) {
+        for (int e = t; e < L; e += nthreads) {
+          const int r = e / NS, k = e % NS;
+          base[e] = expi_frac<-1>((uint32_t)(r * k) & (L - 1), L);
+        }
+      } else {
+        for (int e = t; e < R * 64; e += nthreads) {
+          const int r = e / 64, kl = e % 64;
+          base[e] = expi_frac<-1>((uint32_t)(r * kl) & (L - 1), L);
+        }
+        for (int e = t; e < R * (NS / 64); e += nthreads) {
+          const int r = e / (NS / 64), kh = e % (NS / 64);
+          base[R * 64 + e] = expi_frac<-1>((uint32_t)(r * kh * 64) & (L - 1), L);
+        }
+      }
+      build_tw_rev<REV, p + 1>(tw, t, nthreads);
+    }
+  }
+
   template <int LNS, int LR>
   static CSSAR_DEV int swz(int i) {
     constexpr int NS = 1 << LNS;
@@ -89,10 +157,11 @@ struct Engine {
     else { b = g / (N / R); j = g % (N / R); }
   }
 
-  // butterflies of one pass on registers v (E elements: group m at v[m*R .. m*R+R))
+  // butterflies of one pass on registers v (E elements: group m at v[m*R .. m*R+R));
+  // tw = this pass's SMEM twiddle table (required for passes with NS > 1)
   template <int LR, int LNS, int DIR>
-  static CSSAR_DEV void butterflies(float2 (&v)[E], int t) {
-    constexpr int R = 1 << LR, NS = 1 << LNS;
+  static CSSAR_DEV void butterflies(float2 (&v)[E], int t, const float2* tw) {
+    constexpr int R = 1 << LR, NS = 1 << LNS, L = NS * R;
 #pragma unroll
     for (int m = 0; m < E / R; ++m) {
       int b, j;
@@ -100,7 +169,21 @@ struct Engine {
       float2 x[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = v[m * R + r];
-      if constexpr (NS > 1) apply_twiddles<R, DIR>(x, (uint32_t)(j & (NS - 1)), (uint32_t)(NS * R));
+      if constexpr (NS > 1) {
+        const int k = j & (NS - 1);
+        if constexpr (L <= 1024) {
+#pragma unroll
+          for (int r = 1; r < R; ++r) x[r] = DIR < 0 ? cmul(x[r], tw[r * NS + k]) : cmulc(x[r], tw[r * NS + k]);
+        } else {
+          const float2* lo = tw + (k & 63);
+          const float2* hi = tw + R * 64 + (k >> 6);
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const float2 w = cmul(lo[r * 64], hi[r * (NS / 64)]);
+            x[r] = DIR < 0 ? cmul(x[r], w) : cmulc(x[r], w);
+          }
+        }
+      }
       dft<R, DIR>(x);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[m * R + r] = x[r];
@@ -148,47 +231,47 @@ struct Engine {
   // Passes p = P0 .. P-1 of a transform whose first pass input is already in registers.
   // On return the last pass output (natural order, groups j + r N/R_last) is in v.
   template <int DIR, bool REV, int p>
-  static CSSAR_DEV void passes_from(float2* s, float2 (&v)[E], int t) {
+  static CSSAR_DEV void passes_from(float2* s, float2 (&v)[E], int t, const float2* tw) {
     constexpr int LR = lr<REV>(p), LNS = lns<REV>(p);
-    butterflies<LR, LNS, DIR>(v, t);
+    butterflies<LR, LNS, DIR>(v, t, tw + tw_off<REV>(p));
     if constexpr (p + 1 < P) {
       __syncthreads();                 // everyone finished reading the previous exchange
       write<LR, LNS>(s, v, t);
       __syncthreads();
       read<lr<REV>(p + 1), LR, LNS>(s, v, t);
-      passes_from<DIR, REV, p + 1>(s, v, t);
+      passes_from<DIR, REV, p + 1>(s, v, t, tw);
     }
   }
 
   // Load functor: ld(b, j, x) fills x[r] = input element (b, j + r N/R0), R0 = first radix.
   // Store functor: st(b, j, x) consumes output elements (b, j + r N/R_last).
   template <int DIR, class Load, class Store>
-  static CSSAR_DEV void run(float2* s, Load&& ld, Store&& st) {
+  static CSSAR_DEV void run(float2* s, Load&& ld, Store&& st, const float2* tw) {
     const int t = threadIdx.x;
     float2 v[E];
     for_groups<lr<false>(0)>(v, t, ld);
-    passes_from<DIR, false, 0>(s, v, t);
+    passes_from<DIR, false, 0>(s, v, t, tw);
     for_groups<lr<false>(P - 1)>(v, t, st);
   }
 
   // transform(DIR) -> mid -> transform(-DIR), mid acting on natural-order groups in registers
   template <int DIR, class Load, class Mid, class Store>
-  static CSSAR_DEV void conv(float2* s, Load&& ld, Mid&& mid, Store&& st) {
+  static CSSAR_DEV void conv(float2* s, Load&& ld, Mid&& mid, Store&& st, const float2* tw) {
     const int t = threadIdx.x;
     float2 v[E];
     for_groups<lr<false>(0)>(v, t, ld);
-    passes_from<DIR, false, 0>(s, v, t);
+    passes_from<DIR, false, 0>(s, v, t, tw);
     for_groups<lr<false>(P - 1)>(v, t, mid);
-    passes_from<-DIR, true, 0>(s, v, t);
+    passes_from<-DIR, true, 0>(s, v, t, tw);
     for_groups<lr<true>(P - 1)>(v, t, st);
   }
 
   // run() without the Store: the natural-order output groups stay in v (for cluster kernels)
   template <int DIR, class Load>
-  static CSSAR_DEV void run_keep(float2* s, float2 (&v)[E], Load&& ld) {
+  static CSSAR_DEV void run_keep(float2* s, float2 (&v)[E], Load&& ld, const float2* tw) {
     const int t = threadIdx.x;
     for_groups<lr<false>(0)>(v, t, ld);
-    passes_from<DIR, false, 0>(s, v, t);
+    passes_from<DIR, false, 0>(s, v, t, tw);
   }
 
   // write the natural-order output groups of the last pass (radix of pass P-1) unswizzled
@@ -211,7 +294,7 @@ struct Engine {
   // Same as run(), but the first pass reads its input from SMEM in natural order
   // (s[addr(b, i)], unswizzled) — used after a cluster scatter.
   template <int DIR, class Store>
-  static CSSAR_DEV void run_from_smem(float2* s, Store&& st) {
+  static CSSAR_DEV void run_from_smem(float2* s, Store&& st, const float2* tw) {
     const int t = threadIdx.x;
     float2 v[E];
     constexpr int LR0 = lr<false>(0), R0 = 1 << LR0;
@@ -219,7 +302,7 @@ struct Engine {
 #pragma unroll
       for (int r = 0; r < R0; ++r) x[r] = s[addr(b, j + r * (N / R0))];
     });
-    passes_from<DIR, false, 0>(s, v, t);
+    passes_from<DIR, false, 0>(s, v, t, tw);
     for_groups<lr<false>(P - 1)>(v, t, st);
   }
 };

@@ -60,6 +60,7 @@ struct AzArgs {
   int rule;
   float mu;
   float scale;              // 1/sqrt(n_az)
+  const float2* tw;         // precomputed inter-pass twiddle tables of the az engine (global)
 };
 
 struct RgArgs {
@@ -67,6 +68,7 @@ struct RgArgs {
   const RowCoef* coef;
   int row_base;             // global Doppler row of data row 0
   float scale;              // 1/n_rg
+  const float2* tab;        // [exp(2 pi i h/256), h < 256 | inter-pass twiddle tables] (global)
 };
 
 enum AzMode : int {
@@ -88,6 +90,11 @@ cudaError_t launch_select(int n_threads_hint, float2* b, long long n, long long 
 cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,
                               cudaStream_t s);
 cudaError_t launch_finalize(float2* b, long long n, int thr, const SelState* st, cudaStream_t s);
+// precomputed SMEM tables (filled once per plan, copied into SMEM by each CTA)
+size_t rg_table_count(int log_nrg);
+cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s);
+size_t az_table_count(int log_naz);
+cudaError_t az_table_fill(int log_naz, float2* dst, cudaStream_t s);
 cudaError_t launch_pack_mask(const uint8_t* m, uint32_t* bits, long long rows, long long cols, cudaStream_t s);
 
 }  // namespace cssar

@@ -14,7 +14,9 @@ struct RgCfg {
 #define CSSAR_RG_MINB 2
 #endif
   static constexpr int MINB = LOGN >= 14 ? 1 : CSSAR_RG_MINB;   // resident CTAs per SM (register cap)
-  static constexpr size_t SMEM = sizeof(float2) * (N * B + 256);
+  using En = Engine<LOGN, B, T, false, E>;
+  static constexpr int TAB = 256 + En::TW_TOTAL;                // phase table + twiddle tables
+  static constexpr size_t SMEM = sizeof(float2) * (N * B + TAB);
 };
 
 // GBODY: Phi3* -> F -> Phi2* -> F^-1 -> Phi1*  (inverse of the focusing steps)
@@ -22,7 +24,7 @@ struct RgCfg {
 template <int LOGN, bool GBODY>
 __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_kernel(const RgArgs a) {
   using C = RgCfg<LOGN>;
-  using En = Engine<LOGN, C::B, C::T, false, C::E>;
+  using En = typename C::En;
   constexpr int N = C::N;
   constexpr int R0 = 1 << En::template lr<false>(0);
   constexpr int RL = 1 << En::template lr<false>(En::P - 1);
@@ -30,7 +32,8 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   float2* s = reinterpret_cast<float2*>(smem4);
   const int row0 = blockIdx.x * C::B;
   float2* tab = s + N * C::B;                 // exp(2 pi i h / 256) for the phase generator
-  init_expi_table(tab, threadIdx.x, C::T);
+  const float2* tw = tab + 256;               // inter-pass twiddles
+  copy_table(tab, a.tab, C::TAB, threadIdx.x, C::T);
   __syncthreads();
   float2* __restrict__ data = a.data;
 
@@ -54,7 +57,32 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
 #pragma unroll
     for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r] * a.scale;
   };
-  En::template conv<-1>(s, ld, mid, st);
+  En::template conv<-1>(s, ld, mid, st, tw);
+}
+
+template <int LOGN>
+__global__ void rg_table_kernel(float2* dst) {
+  using C = RgCfg<LOGN>;
+  init_expi_table(dst, threadIdx.x, blockDim.x);
+  C::En::build_tw(dst + 256, threadIdx.x, blockDim.x);
+}
+
+size_t rg_table_count(int log_nrg) {
+  switch (log_nrg) {
+#define RGT(L) case L: return RgCfg<L>::TAB;
+    RGT(7) RGT(8) RGT(9) RGT(10) RGT(11) RGT(12) RGT(13) RGT(14)
+#undef RGT
+    default: return 0;
+  }
+}
+
+cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s) {
+  switch (log_nrg) {
+#define RGT(L) case L: rg_table_kernel<L><<<1, 256, 0, s>>>(dst); return cudaGetLastError();
+    RGT(7) RGT(8) RGT(9) RGT(10) RGT(11) RGT(12) RGT(13) RGT(14)
+#undef RGT
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <int LOGN, bool GB>
