@@ -2,6 +2,7 @@
 // thread-block clusters + DSMEM for long columns.  Instantiated per log2(n_az) in az_*.cu.
 #pragma once
 #include "device_ops.cuh"
+#include "cluster.cuh"
 
 namespace cssar {
 
@@ -58,12 +59,12 @@ template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR) ? -1 : +1;   // first transform direction
 
-  CSSAR_DEV static float2 pro(const AzArgs& a, int row, int col, size_t idx) {
-    float2 v = a.in[idx];
+  // prologue on a loaded input value (loads are issued for a whole group first)
+  CSSAR_DEV static float2 pro(const AzArgs& a, int row, int col, float2 v, uint32_t s2, float sig) {
     if constexpr (MODE == AZ_FWD_MASK) {
       if (!mask_bit(a.mask, a.mask_words, row, col)) v = make_float2(0.f, 0.f);
     }
-    if constexpr (MODE == AZ_FWD_THR) v = threshold(v, a.st->sigma2_bits, a.st->sigma, a.thr);
+    if constexpr (MODE == AZ_FWD_THR) v = threshold(v, s2, sig, a.thr);
     return v;
   }
 
@@ -135,8 +136,7 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
   extern __shared__ float4 smem4[];
   float2* tw = reinterpret_cast<float2*>(smem4);      // inter-pass twiddle tables
   float2* s = tw + Cf::TW;                             // panel data
-  copy_table(tw, a.tw, Cf::TW, threadIdx.x, Cf::T);
-  __syncthreads();
+  copy_table_async(tw, a.tw, Cf::TW, threadIdx.x, Cf::T);   // waited for before the first exchange
   int rank = 0;
   if constexpr (C > 1) rank = (int)cg::this_cluster().block_rank();
   const int col0 = (blockIdx.x / C) * W;
@@ -160,13 +160,22 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
   }
   float racc = 0.f;
 
-  // DIT-first input rows: local index m -> global row rank + C m
+  uint32_t s2 = 0u;
+  float sig = 0.f;
+  if constexpr (MODE == AZ_FWD_THR) {
+    s2 = a.st->sigma2_bits;
+    sig = a.st->sigma;
+  }
+  // DIT-first input rows: local index m -> global row rank + C m; all loads of a group are
+  // issued before the prologue arithmetic
   auto ld = [&](int w, int j, float2* x) {
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
       const int row = rank + C * (j + r * (M / R0));
-      x[r] = Ops::pro(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+      x[r] = a.in[(size_t)row * n_rg + col0 + w];
     }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) x[r] = Ops::pro(a, rank + C * (j + r * (M / R0)), col0 + w, x[r], s2, sig);
   };
 
   if constexpr (C == 1) {

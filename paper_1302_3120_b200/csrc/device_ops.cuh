@@ -27,17 +27,17 @@ CSSAR_DEV uint32_t mag2_bits(float2 v) {
 // soft (eq. 9) or half (q = 1/2) shrink of the magnitude, phase preserved.
 CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
   const uint32_t u = mag2_bits(b);
-  if (u <= s2bits) return make_float2(0.f, 0.f);
-  if (sigma == 0.f) return b;
-  const float a = sqrtf(__uint_as_float(u));
+  const float a2 = __uint_as_float(u);
   float f;
   if (thr == THR_SOFT) {
-    f = 1.0f - sigma / a;
+    f = fmaf(-sigma, rsqrtf(a2), 1.0f);                   // 1 - sigma/|b|   (sigma = 0 -> 1)
   } else {
-    const float ratio = sigma / a;
+    const float ratio = sigma * rsqrtf(a2);
     const float phi = acosf(0.70710678118654752f * ratio * sqrtf(ratio));
     f = (2.0f / 3.0f) * (1.0f + cosf(2.09439510239319549f - (2.0f / 3.0f) * phi));
+    f = sigma == 0.f ? 1.0f : f;
   }
+  f = (u > s2bits) ? f : 0.0f;                             // strict survival on the |b|^2 pattern
   return make_float2(b.x * f, b.y * f);
 }
 

@@ -19,6 +19,7 @@
 // log2(NS R); reader and writer agree on the swizzle of each exchange.
 #pragma once
 #include "common.cuh"
+#include "cluster.cuh"
 
 namespace cssar {
 
@@ -233,6 +234,7 @@ struct Engine {
   template <int DIR, bool REV, int p>
   static CSSAR_DEV void passes_from(float2* s, float2 (&v)[E], int t, const float2* tw) {
     constexpr int LR = lr<REV>(p), LNS = lns<REV>(p);
+    if constexpr (p == 0 && !REV) cp_async_wait_all();   // async table staging (no-op if none)
     butterflies<LR, LNS, DIR>(v, t, tw + tw_off<REV>(p));
     if constexpr (p + 1 < P) {
       __syncthreads();                 // everyone finished reading the previous exchange

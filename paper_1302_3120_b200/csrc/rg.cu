@@ -1,5 +1,6 @@
 // Range sweeps (S2 G body, S4 M body): one or more range lines per CTA.
 #include "device_ops.cuh"
+#include "cluster.cuh"
 
 namespace cssar {
 
@@ -33,31 +34,38 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   const int row0 = blockIdx.x * C::B;
   float2* tab = s + N * C::B;                 // exp(2 pi i h / 256) for the phase generator
   const float2* tw = tab + 256;               // inter-pass twiddles
-  copy_table(tab, a.tab, C::TAB, threadIdx.x, C::T);
-  __syncthreads();
+  const int t = threadIdx.x;
+  copy_table_async(tab, a.tab, C::TAB, t, C::T);
   float2* __restrict__ data = a.data;
+  constexpr int LR0 = En::template lr<false>(0), LRL = En::template lr<false>(En::P - 1);
 
-  auto ld = [&](int b, int j, float2* x) {
+  float2 v[En::E];
+  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // raw row loads
     const float2* src = data + (size_t)(row0 + b) * N;
 #pragma unroll
     for (int r = 0; r < R0; ++r) x[r] = src[j + r * (N / R0)];
+  });
+  cp_async_wait_all();
+  __syncthreads();                                                        // tables visible
+  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // prologue phase
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
     phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
-  };
-  auto mid = [&](int b, int j, float2* x) {
+  });
+  En::template passes_from<-1, false, 0>(s, v, t, tw);                   // range FFT
+  En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[1];
     // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
     phase_apply<RL / 2, N / RL, GBODY>(tab, q, j, x);
     phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
-  };
-  auto st = [&](int b, int j, float2* x) {
+  });
+  En::template passes_from<+1, true, 0>(s, v, t, tw);                    // range IFFT
+  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
     phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     float2* dst = data + (size_t)(row0 + b) * N;
 #pragma unroll
     for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r] * a.scale;
-  };
-  En::template conv<-1>(s, ld, mid, st, tw);
+  });
 }
 
 template <int LOGN>
