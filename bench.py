@@ -258,6 +258,7 @@ def main():
                                "frac": iter_ach / peak, "bytes_per_sample": ITER_BYTES_PER_SAMPLE},
         "stages_ms": stages,
         "gpu_launches": args.steps * (10 if cfg.rule == "k" else 6) + 2,
+        "select_fallbacks": plan.debug_fallbacks(),
         "clocks": clocks,
     }
 

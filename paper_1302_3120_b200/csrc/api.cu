@@ -37,7 +37,8 @@ struct cssar_plan_s {
   int sm_count = 148;
   RowCoef* d_coef = nullptr;
   float2* d_rg_tab = nullptr;     // phase exp table + range-engine twiddles
-  float2* d_az_tab = nullptr;     // azimuth-engine twiddles
+  float2* d_az_tab = nullptr;     // azimuth-engine twiddles (head / tail / operator kernels)
+  float2* d_az_tab_r = nullptr;   // azimuth-engine twiddles (residual kernel)
   SelState* d_st = nullptr;
   uint32_t* d_hist = nullptr;
   uint32_t* d_hist_full = nullptr;
@@ -207,7 +208,9 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   // S3: F_eta^-1 ; r = Theta o (Y - G X_i) ; F_eta
   a.in = pl->U;
   a.out = pl->U;
+  a.tw = pl->d_az_tab_r;
   CUDA_TRY(launch_az(pl->log_naz, AZ_RESID, a.n_rg, a, s));
+  a.tw = pl->d_az_tab;
   MARK(3);
   // S4: M body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
@@ -277,9 +280,11 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
       cudaMalloc(&pl->d_log, sizeof(IterLogDev) * kLogCap) != cudaSuccess ||
       cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&pl->d_rg_tab, sizeof(float2) * rg_table_count(pl->log_nrg)) != cudaSuccess ||
-      cudaMalloc(&pl->d_az_tab, sizeof(float2) * (az_table_count(pl->log_naz) + 2)) != cudaSuccess ||
+      cudaMalloc(&pl->d_az_tab, sizeof(float2) * (az_table_count(pl->log_naz, false) + 2)) != cudaSuccess ||
+      cudaMalloc(&pl->d_az_tab_r, sizeof(float2) * (az_table_count(pl->log_naz, true) + 2)) != cudaSuccess ||
       rg_table_fill(pl->log_nrg, pl->d_rg_tab, pl->cap_stream) != cudaSuccess ||
-      az_table_fill(pl->log_naz, pl->d_az_tab, pl->cap_stream) != cudaSuccess ||
+      az_table_fill(pl->log_naz, false, pl->d_az_tab, pl->cap_stream) != cudaSuccess ||
+      az_table_fill(pl->log_naz, true, pl->d_az_tab_r, pl->cap_stream) != cudaSuccess ||
       cudaStreamSynchronize(pl->cap_stream) != cudaSuccess) {
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
@@ -302,6 +307,7 @@ int cssar_plan_destroy(cssar_plan pl) {
   cudaFree(pl->d_coef);
   cudaFree(pl->d_rg_tab);
   cudaFree(pl->d_az_tab);
+  cudaFree(pl->d_az_tab_r);
   cudaFree(pl->d_st);
   cudaFree(pl->d_hist);
   cudaFree(pl->d_hist_full);

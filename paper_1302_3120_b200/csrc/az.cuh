@@ -7,24 +7,31 @@
 namespace cssar {
 
 // ------------------------------------------------------------------ azimuth sweeps
-template <int LOGN>
+// R = configuration for the residual kernel (two transforms; more registers)
+template <int LOGN, bool R>
 struct AzCfg {
   // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
   // 4096-8192 complex64 per CTA (32-64 KB SMEM), E elements per thread
-  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
-  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : 4;
+  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? (R ? 16 : 8) : 16;
+  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 13 ? 8 : 4;
   static constexpr int E = 16;
 };
 #if defined(CSSAR_AZ13_C)
 template <>
-struct AzCfg<13> {
+struct AzCfg<13, false> {
   static constexpr int C = CSSAR_AZ13_C, W = CSSAR_AZ13_W, E = CSSAR_AZ13_E;
 };
 #endif
+#if defined(CSSAR_AZ13R_C)
+template <>
+struct AzCfg<13, true> {
+  static constexpr int C = CSSAR_AZ13R_C, W = CSSAR_AZ13R_W, E = CSSAR_AZ13R_E;
+};
+#endif
 
-template <int LOGN>
+template <int LOGN, bool R = false>
 struct AzShape {
-  using P = AzCfg<LOGN>;
+  using P = AzCfg<LOGN, R>;
   static constexpr int C = P::C, W = P::W, E = P::E;
   static constexpr int LOGM = LOGN - ilog2c(C);
   static constexpr int M = 1 << LOGM;
@@ -123,9 +130,10 @@ struct AzOps {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape<LOGN>::MINB > 2) ? 2 : AzShape<LOGN>::MINB)
+__global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
+                                  (MODE == AZ_RESID && AzShape<LOGN, true>::MINB > 2) ? 2 : AzShape<LOGN, MODE == AZ_RESID>::MINB)
     az_kernel(const AzArgs a) {
-  using Cf = AzShape<LOGN>;
+  using Cf = AzShape<LOGN, MODE == AZ_RESID>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
   using En = typename Cf::En;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(AzShape<LOGN>::T, (MODE == AZ_RESID && AzShape
 
 template <int LOGN, int MODE>
 static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
-  using Cf = AzShape<LOGN>;
+  using Cf = AzShape<LOGN, MODE == AZ_RESID>;
   auto k = az_kernel<LOGN, MODE>;
   const size_t smem = (MODE == AZ_TAIL) ? Cf::SMEM_TAIL : (MODE == AZ_RESID) ? Cf::SMEM_RESID : Cf::SMEM_FFT;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -370,17 +378,18 @@ static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int LOGN>
+template <int LOGN, bool R>
 __global__ void az_table_kernel(float2* dst) {
-  AzShape<LOGN>::En::build_tw(dst, threadIdx.x, blockDim.x);
+  AzShape<LOGN, R>::En::build_tw(dst, threadIdx.x, blockDim.x);
 }
 
 template <int LOGN>
-size_t az_table_count_t() { return (size_t)AzShape<LOGN>::TW; }
+size_t az_table_count_t(bool resid) { return resid ? (size_t)AzShape<LOGN, true>::TW : (size_t)AzShape<LOGN, false>::TW; }
 
 template <int LOGN>
-cudaError_t az_table_fill_t(float2* dst, cudaStream_t s) {
-  az_table_kernel<LOGN><<<1, 256, 0, s>>>(dst);
+cudaError_t az_table_fill_t(bool resid, float2* dst, cudaStream_t s) {
+  if (resid) az_table_kernel<LOGN, true><<<1, 256, 0, s>>>(dst);
+  else az_table_kernel<LOGN, false><<<1, 256, 0, s>>>(dst);
   return cudaGetLastError();
 }
 

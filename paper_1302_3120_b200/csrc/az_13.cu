@@ -1,6 +1,6 @@
 #include "az.cuh"
 namespace cssar {
 template cudaError_t az_dispatch_mode<13>(int, int, const AzArgs&, cudaStream_t);
-template size_t az_table_count_t<13>();
-template cudaError_t az_table_fill_t<13>(float2*, cudaStream_t);
+template size_t az_table_count_t<13>(bool);
+template cudaError_t az_table_fill_t<13>(bool, float2*, cudaStream_t);
 }  // namespace cssar

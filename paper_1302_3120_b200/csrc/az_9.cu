@@ -1,6 +1,6 @@
 #include "az.cuh"
 namespace cssar {
 template cudaError_t az_dispatch_mode<9>(int, int, const AzArgs&, cudaStream_t);
-template size_t az_table_count_t<9>();
-template cudaError_t az_table_fill_t<9>(float2*, cudaStream_t);
+template size_t az_table_count_t<9>(bool);
+template cudaError_t az_table_fill_t<9>(bool, float2*, cudaStream_t);
 }  // namespace cssar

@@ -18,7 +18,7 @@ enum Rule : int { RULE_K = 1, RULE_LAMBDA = 2 };
 constexpr int HIST_BITS = 11;                  // top bits of the 31-bit |b|^2 pattern
 constexpr int HIST_BINS = 1 << HIST_BITS;      // 2048 bins, 8 per octave of |b|^2
 constexpr int HIST_SHIFT = 31 - HIST_BITS;     // 20
-constexpr int FLOOR_MARGIN = 24;               // bins below the last sigma^2 bin still counted
+constexpr int FLOOR_MARGIN = 8;                // bins below the last sigma^2 bin still counted
 constexpr int CAND_MARGIN = 2;                 // candidate window half-width (bins)
 
 // Device-resident solver state (one per plan); no host round trip inside the loop.
@@ -93,8 +93,8 @@ cudaError_t launch_finalize(float2* b, long long n, int thr, const SelState* st,
 // precomputed SMEM tables (filled once per plan, copied into SMEM by each CTA)
 size_t rg_table_count(int log_nrg);
 cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s);
-size_t az_table_count(int log_naz);
-cudaError_t az_table_fill(int log_naz, float2* dst, cudaStream_t s);
+size_t az_table_count(int log_naz, bool resid);
+cudaError_t az_table_fill(int log_naz, bool resid, float2* dst, cudaStream_t s);
 cudaError_t launch_pack_mask(const uint8_t* m, uint32_t* bits, long long rows, long long cols, cudaStream_t s);
 
 }  // namespace cssar

@@ -6,9 +6,9 @@ namespace cssar {
 template <int LOGN>
 cudaError_t az_dispatch_mode(int mode, int n_rg, const AzArgs& a, cudaStream_t s);
 template <int LOGN>
-size_t az_table_count_t();
+size_t az_table_count_t(bool resid);
 template <int LOGN>
-cudaError_t az_table_fill_t(float2* dst, cudaStream_t s);
+cudaError_t az_table_fill_t(bool resid, float2* dst, cudaStream_t s);
 extern template cudaError_t az_dispatch_mode<7>(int, int, const AzArgs&, cudaStream_t);
 extern template cudaError_t az_dispatch_mode<8>(int, int, const AzArgs&, cudaStream_t);
 extern template cudaError_t az_dispatch_mode<9>(int, int, const AzArgs&, cudaStream_t);
@@ -19,18 +19,18 @@ extern template cudaError_t az_dispatch_mode<13>(int, int, const AzArgs&, cudaSt
 extern template cudaError_t az_dispatch_mode<14>(int, int, const AzArgs&, cudaStream_t);
 extern template cudaError_t az_dispatch_mode<15>(int, int, const AzArgs&, cudaStream_t);
 
-size_t az_table_count(int log_naz) {
+size_t az_table_count(int log_naz, bool resid) {
   switch (log_naz) {
-#define AZT(L) case L: return az_table_count_t<L>();
+#define AZT(L) case L: return az_table_count_t<L>(resid);
     AZT(7) AZT(8) AZT(9) AZT(10) AZT(11) AZT(12) AZT(13) AZT(14) AZT(15)
 #undef AZT
     default: return 0;
   }
 }
 
-cudaError_t az_table_fill(int log_naz, float2* dst, cudaStream_t s) {
+cudaError_t az_table_fill(int log_naz, bool resid, float2* dst, cudaStream_t s) {
   switch (log_naz) {
-#define AZT(L) case L: return az_table_fill_t<L>(dst, s);
+#define AZT(L) case L: return az_table_fill_t<L>(resid, dst, s);
     AZT(7) AZT(8) AZT(9) AZT(10) AZT(11) AZT(12) AZT(13) AZT(14) AZT(15)
 #undef AZT
     default: return cudaErrorInvalidValue;
