@@ -1,6 +1,7 @@
 // Azimuth sweeps (S1 head, S3 residual, S5 tail, operator heads/tails): column panels,
 // thread-block clusters + DSMEM for long columns.  Instantiated per log2(n_az) in az_*.cu.
 #pragma once
+#include <cuda.h>
 #include "device_ops.cuh"
 #include "cluster.cuh"
 
@@ -11,39 +12,52 @@ namespace cssar {
 template <int LOGN, bool R>
 struct AzCfg {
   // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
-  // 4096-8192 complex64 per CTA (32-64 KB SMEM), E elements per thread
-  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? (R ? 16 : 8) : 16;
-  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 13 ? 8 : 4;
+  // C > 1: persistent cluster kernel with NS TMA stages of M*W complex64 per CTA
+  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
+  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 10 ? 4 : LOGN <= 14 ? 8 : 4;
   static constexpr int E = 16;
+  static constexpr int NS = R ? 1 : 2;       // RESID also holds the receive + scatter buffers
 };
 #if defined(CSSAR_AZ13_C)
 template <>
 struct AzCfg<13, false> {
-  static constexpr int C = CSSAR_AZ13_C, W = CSSAR_AZ13_W, E = CSSAR_AZ13_E;
+  static constexpr int C = CSSAR_AZ13_C, W = CSSAR_AZ13_W, E = CSSAR_AZ13_E, NS = CSSAR_AZ13_NS;
 };
 #endif
 #if defined(CSSAR_AZ13R_C)
 template <>
 struct AzCfg<13, true> {
-  static constexpr int C = CSSAR_AZ13R_C, W = CSSAR_AZ13R_W, E = CSSAR_AZ13R_E;
+  static constexpr int C = CSSAR_AZ13R_C, W = CSSAR_AZ13R_W, E = CSSAR_AZ13R_E, NS = CSSAR_AZ13R_NS;
 };
 #endif
 
-template <int LOGN, bool R = false>
+template <int LOGN, bool R = false, int NSO = 0>
 struct AzShape {
   using P = AzCfg<LOGN, R>;
-  static constexpr int C = P::C, W = P::W, E = P::E;
+  static constexpr int C = P::C, W = P::W, E = P::E, NS = NSO > 0 ? NSO : P::NS;
   static constexpr int LOGM = LOGN - ilog2c(C);
   static constexpr int M = 1 << LOGM;
   static constexpr int T = M * W / E;
   static constexpr int MINB = T <= 128 ? 4 : T <= 256 ? (E == 32 ? 2 : 3) : (E == 32 ? 1 : 2);
-  static constexpr int NBUF = C > 1 ? 2 : 1;               // RESID double-buffers the scatter
   using En = Engine<LOGM, W, T, true, E>;
   static constexpr int TW = En::TW_TOTAL;
-  static constexpr size_t SMEM_FFT = sizeof(float2) * (M * W + TW);
   static constexpr int CAND_SMEM = 1024;
+  // C == 1 (az_kernel): [twiddles | panel | (TAIL) hist, candidates, counters]
+  static constexpr size_t SMEM_FFT = sizeof(float2) * (M * W + TW);
   static constexpr size_t SMEM_TAIL = SMEM_FFT + sizeof(uint32_t) * (HIST_BINS + CAND_SMEM + 4);
-  static constexpr size_t SMEM_RESID = SMEM_FFT + sizeof(float2) * M * W * (NBUF - 1);
+  static constexpr size_t SMEM_RESID = SMEM_FFT;
+  // C > 1 (az_cluster_kernel): [NS stages | receive buffer | (RESID) scatter buffer | twiddles | mbarriers |
+  // (TAIL) hist, candidates, counters], 1024-byte aligned stages
+  static constexpr int BM = M < 256 ? M : 256;             // TMA box rows (box dims <= 256)
+  static constexpr uint32_t STAGE_BYTES = (uint32_t)(sizeof(float2) * M * W);
+  static constexpr size_t CL_TW_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R ? 1 : 0));
+  static constexpr int LO = (LOGN + 1) / 2;                      // cluster twiddle table split
+  static constexpr int CTW = (1 << LO) + (1 << (LOGN - LO));      // lo[2^LO] | hi[N / 2^LO]
+  static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TW + 15) / 16) * 16;
+  static constexpr size_t CL_BAR_OFF = CL_CTW_OFF + sizeof(float2) * CTW;
+  static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 16 + 8;
+  static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (HIST_BINS + CAND_SMEM + 4));
+  static constexpr int CL_MINB = T <= 256 ? 2 : 1;
 };
 
 struct TailCtx {
@@ -186,7 +200,8 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
     for (int r = 0; r < R0; ++r) x[r] = Ops::pro(a, rank + C * (j + r * (M / R0)), col0 + w, x[r], s2, sig);
   };
 
-  if constexpr (C == 1) {
+  static_assert(C == 1, "cluster shapes use az_cluster_kernel");
+  {
     if constexpr (MODE == AZ_RESID) {
       auto mid = [&](int w, int j, float2* x) {
         Aux ax[RL];
@@ -221,96 +236,6 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
         }
       };
       En::template run<Ops::DIR>(s, ld, st, tw);
-    }
-  } else {
-    auto cluster = cg::this_cluster();
-    float2 v[E];
-    En::template run_keep<Ops::DIR>(s, v, ld, tw);
-    En::store_natural(s, v);
-    cluster.sync();
-    // gather: this rank owns local output indices k in [rank M/C, (rank+1) M/C)
-    constexpr int PT = E / C > 0 ? E / C : 1;       // (k, w) pairs per thread
-    static_assert((M / C) * W == PT * T, "cluster gather shape");
-    float2 z[PT][C];
-#pragma unroll
-    for (int p = 0; p < PT; ++p) {
-      const int pr = p * T + t;
-      const int w = pr % W, k = rank * (M / C) + pr / W;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const float2* rs = cluster.map_shared_rank(s, c);
-        z[p][c] = rs[k * W + w];
-      }
-    }
-    if constexpr (MODE != AZ_RESID) cluster.barrier_arrive();    // done reading remote SMEM
-    // auxiliary inputs of the elements this thread finalises (rows k + M q)
-    Aux ax[PT][C];
-    if constexpr (MODE == AZ_RESID || MODE == AZ_TAIL || MODE == AZ_INV_MASK) {
-#pragma unroll
-      for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
-#pragma unroll
-        for (int q = 0; q < C; ++q) {
-          const int row = k + M * q;
-          ax[p][q] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
-        }
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < PT; ++p) {
-      const int pr = p * T + t;
-      const int k = rank * (M / C) + pr / W;
-      apply_twiddles<C, Ops::DIR>(z[p], (uint32_t)k, (uint32_t)N);   // w_N^{c k}
-      dft<C, Ops::DIR>(z[p]);                         // z[q] = X[k + M q]
-    }
-    if constexpr (MODE == AZ_RESID) {
-#pragma unroll
-      for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int k = rank * (M / C) + pr / W;
-#pragma unroll
-        for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
-        // forward DIF first stage: y_q = (sum_q' x_q' w_C^{q q'}) w_N^{q k}
-        dft<C, -1>(z[p]);
-        apply_twiddles<C, -1>(z[p], (uint32_t)k, (uint32_t)N);       // w_N^{-q k}
-      }
-      // scatter into the second SMEM buffer of CTA q (no barrier needed against the gathers,
-      // which read the first buffer)
-      float2* s2 = s + M * W;
-#pragma unroll
-      for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
-#pragma unroll
-        for (int q = 0; q < C; ++q) {
-          float2* rs = cluster.map_shared_rank(s2, q);
-          rs[k * W + w] = z[p][q];
-        }
-      }
-      cluster.sync();
-      s = s2;
-      // local forward FFT of y_rank: X[C m + rank] -> row rank + C m
-      auto st = [&](int w, int j, float2* x) {
-#pragma unroll
-        for (int r = 0; r < RL; ++r) {
-          const int row = rank + C * (j + r * (M / RL));
-          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
-        }
-      };
-      En::template run_from_smem<-1>(s, st, tw);
-    } else {
-#pragma unroll
-      for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
-#pragma unroll
-        for (int q = 0; q < C; ++q) {
-          const int row = k + M * q;
-          Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
-        }
-      }
-      cluster.barrier_wait();                          // keep SMEM alive for remote readers
     }
   }
 
@@ -350,9 +275,377 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
   }
 }
 
+
+// ------------------------------------------------------------------ persistent cluster kernel
+// C > 1: a cluster of C CTAs owns whole columns.  CTA `rank` holds the M rows rank + C m of a
+// panel of W adjacent range bins; TMA (3-D tensor map {col, rank, m}) streams each panel into
+// one of NS SMEM stages while the previous panel is transformed.  Per panel:
+//   local M-point FFT (DIT-first: rows rank + C m) in the stage buffer -> cluster barrier ->
+//   DSMEM gather of the C partial transforms of output rows k + M q (k in this rank's M/C
+//   block) -> twiddle w_N^{c k} + radix-C DFT -> epilogue -> (RESID: DIF radix-C + DSMEM
+//   scatter into the peers' scatter buffers -> cluster barrier -> local FFT -> rows rank + C m).
+// The stage is refilled (TMA, panel + NS clusters ahead) once every peer has finished reading
+// it (split cluster barrier after the gather).  Epilogue inputs (Y, mask words, b) of a panel
+// are loaded into registers before its FFT so their latency hides behind the transform.
+// Cluster barriers without the release fence: a release arrive compiles to MEMBAR.ALL.GPU,
+// which would wait for every outstanding epilogue store.  Ordering is provided instead by
+// (a) __syncthreads() before the arrive (drains this CTA's STS into SMEM) for data the peers
+// read after the barrier, and (b) consuming every DSMEM-loaded value before arriving "done
+// reading"; DSMEM scatters complete on an mbarrier (st.async ... complete_tx).
+CSSAR_DEV void cl_arrive() { asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory"); }
+CSSAR_DEV void cl_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
+CSSAR_DEV void cl_arrive_rel() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+CSSAR_DEV void cl_sync() { cl_arrive(); cl_wait(); }
+
+// Force every DSMEM-loaded value to have arrived before the next memory operation (an empty
+// asm does not: no instruction would read the registers).  The values feed a compare that
+// predicates a (never taken) SMEM store, which cannot move across the following asm volatile.
+template <int PT, int C>
+CSSAR_DEV void consume(const float2 (&z)[PT][C], uint32_t* sink) {
+  float acc = 0.f;
+#pragma unroll
+  for (int p = 0; p < PT; ++p)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc += z[p][c].x + z[p][c].y;
+  if (acc == 1.2345e-38f) *reinterpret_cast<volatile uint32_t*>(sink) = 0u;
+}
+
+CSSAR_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// x[c] *= w_N^{DIR c k}, c = 1..C-1, each power read directly from the two-level SMEM table
+// lo[l] = w_N^l, hi[h] = w_N^{h 2^LO} (one product: at most ~1.5 ulp, no recurrences)
+template <int C, int DIR, int LOGN, int LO>
+CSSAR_DEV void cluster_twiddles(float2* x, uint32_t k, const float2* ctw) {
+  constexpr uint32_t NM = (1u << LOGN) - 1u, LM = (1u << LO) - 1u;
+#pragma unroll
+  for (int c = 1; c < C; ++c) {
+    const uint32_t m = ((uint32_t)c * k) & NM;
+    const float2 w = cmul(ctw[m & LM], ctw[(1u << LO) + (m >> LO)]);
+    x[c] = DIR < 0 ? cmul(x[c], w) : cmulc(x[c], w);
+  }
+}
+
+// async DSMEM store that signals the destination CTA's mbarrier (same SMEM offset mapped)
+CSSAR_DEV void st_async_cluster(uint32_t raddr, float2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "f"(v.x), "f"(v.y), "r"(rbar)
+               : "memory");
+}
+
+CSSAR_DEV void mbar_wait_cta(const uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+template <int LOGN, int MODE>
+using AzClShape = AzShape<LOGN, MODE == AZ_RESID, MODE == AZ_TAIL ? 1 : 0>;
+
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
+    az_cluster_kernel(const AzArgs a, const __grid_constant__ CUtensorMap tm) {
+  using Cf = AzClShape<LOGN, MODE>;
+  constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E, NS = Cf::NS, BM = Cf::BM;
+  constexpr int N = M * C;
+  constexpr bool RES = MODE == AZ_RESID;
+  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_TAIL || MODE == AZ_INV_MASK;
+  static_assert(C > 1, "cluster kernel");
+  using En = typename Cf::En;
+  using Ops = AzOps<MODE>;
+  constexpr int R0 = 1 << En::template lr<false>(0);
+  constexpr int RL = 1 << En::template lr<false>(En::P - 1);
+  constexpr int PT = E / C > 0 ? E / C : 1;       // (k, w) pairs per thread in the gather
+  static_assert((M / C) * W == PT * T, "cluster gather shape");
+
+  extern __shared__ float4 smem4[];
+  // 1024-byte aligned base by offsetting the __shared__ pointer itself (an integer round trip
+  // would lose the shared address space and turn every SMEM access into a generic one)
+  char* base = reinterpret_cast<char*>(smem4) + ((1024u - (smem_u32(smem4) & 1023u)) & 1023u);
+  float2* stages = reinterpret_cast<float2*>(base);
+  float2* rbuf = stages + (size_t)NS * M * W;                      // pushed partial transforms [c][k][w]
+  float2* xbuf = rbuf + (size_t)M * W;                              // RESID scatter target
+  float2* tw = reinterpret_cast<float2*>(base + Cf::CL_TW_OFF);
+  float2* ctw = reinterpret_cast<float2*>(base + Cf::CL_CTW_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + Cf::CL_BAR_OFF);
+  uint64_t* rfull = full + NS;                                     // pushes landed in rbuf
+  uint64_t* xfull = full + NS + 1;                                 // RESID scatter landed in xbuf
+  uint32_t* misc = reinterpret_cast<uint32_t*>(base + Cf::CL_MISC_OFF);   // [0..31] reduce, [32] base
+  const int t = threadIdx.x;
+  const int rank = (int)cluster_rank();
+  const int cid = blockIdx.x / C, ncl = gridDim.x / C;
+  const int n_rg = a.n_rg;
+  const int npan = n_rg / W;
+
+  copy_table_async(tw, a.tw, Cf::TW, t, T);     // waited for in the first FFT pass
+  for (int i = t; i < Cf::CTW; i += T) {         // exact (sincospif) cluster twiddle tables
+    const uint32_t m = i < (1 << Cf::LO) ? (uint32_t)i : (uint32_t)(i - (1 << Cf::LO)) << Cf::LO;
+    ctw[i] = expi_frac<-1>(m, (uint32_t)N);
+  }
+  TailCtx tc{};
+  if constexpr (MODE == AZ_TAIL) {
+    tc.shist = misc + 64;
+    tc.scand = tc.shist + HIST_BINS;
+    tc.scount = tc.scand + Cf::CAND_SMEM;
+    for (int i = t; i < HIST_BINS; i += T) tc.shist[i] = 0u;
+    if (t < 4) tc.scount[t] = 0u;
+    tc.floor_bin = a.st->floor_bin;
+    tc.cand_lo = a.st->cand_lo;
+    tc.cand_hi = a.st->cand_hi;
+    tc.s2bits = a.st->sigma2_bits;
+    tc.s2fixed = a.st->sigma2_fixed_bits;
+    tc.sigma = a.st->sigma;
+  }
+  uint32_t s2 = 0u;
+  float sig = 0.f;
+  if constexpr (MODE == AZ_FWD_THR) {
+    s2 = a.st->sigma2_bits;
+    sig = a.st->sigma;
+  }
+  float racc = 0.f;
+
+  auto issue = [&](int panel, int sidx) {       // one thread: arm the stage barrier, M/BM boxes
+    const uint32_t bar = smem_u32(&full[sidx]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(Cf::STAGE_BYTES)
+                 : "memory");
+    float2* dst = stages + (size_t)sidx * M * W;
+#pragma unroll
+    for (int bx = 0; bx < M / BM; ++bx) {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+          ::"r"(smem_u32(dst + bx * BM * W)), "l"(reinterpret_cast<uint64_t>(&tm)), "r"(panel * W), "r"(rank),
+          "r"(bx * BM), "r"(bar)
+          : "memory");
+    }
+  };
+  if (t == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1u);
+    mbar_init(rfull, 1u);
+    mbar_init(xfull, 1u);
+    mbar_expect_tx(rfull, Cf::STAGE_BYTES);        // armed for the first panel
+    if (RES) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (int i = 0; i < NS; ++i)
+      if (cid + i * ncl < npan) issue(cid + i * ncl, i);
+  }
+  __syncthreads();
+  // barrier initialisation visible cluster-wide before any remote st.async (once per kernel)
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+
+  int it = 0;
+  for (int panel = cid; panel < npan; panel += ncl, ++it) {
+    const int sidx = it % NS;
+    float2* s = stages + (size_t)sidx * M * W;
+    const int col0 = panel * W;
+    const int next = panel + NS * ncl;
+    // epilogue / residual inputs of output rows k + M q (in flight during the FFT)
+    Aux ax[PT][C];
+    if constexpr (AUX) {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const int pr = p * T + t;
+        const int w = pr % W, k = rank * (M / C) + pr / W;
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          const int row = k + M * q;
+          ax[p][q] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+        }
+      }
+    }
+    mbar_wait_cta(&full[sidx], (uint32_t)((it / NS) & 1));
+    // local transform of rows rank + C m (stage layout [m][w] = engine BMINOR layout)
+    auto ld = [&](int w, int j, float2* x) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = s[(j + r * (M / R0)) * W + w];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = Ops::pro(a, rank + C * (j + r * (M / R0)), col0 + w, x[r], s2, sig);
+    };
+    float2 v[E];
+    En::template run_keep<Ops::DIR>(s, v, ld, tw);
+    __syncthreads();                               // stage fully read: refill it NS panels ahead
+    if (t == 0 && next < npan) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(next, sidx);
+    }
+    // push local output k of every column to its owner rank k / (M/C): rbuf[(rank M/C + k%(M/C)) W + w]
+    if (it > 0) cl_wait();                         // owners are done reading their receive buffers
+    {
+      const uint32_t rb = smem_u32(rbuf), bar = smem_u32(rfull);
+      En::template for_groups<En::template lr<false>(En::P - 1)>(v, t, [&](int w, int j, float2* x) {
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int kk = j + r * (M / RL);
+          const uint32_t own = (uint32_t)(kk / (M / C));
+          const uint32_t off = (uint32_t)(((rank * (M / C) + kk % (M / C)) * W + w) * sizeof(float2));
+          st_async_cluster(mapa(rb + off, own), x[r], mapa(bar, own));
+        }
+      });
+    }
+    mbar_wait_cta(rfull, (uint32_t)(it & 1));      // all C partial transforms of our block landed
+    if (t == 0) mbar_expect_tx(rfull, Cf::STAGE_BYTES);   // re-arm for the next panel
+    float2 z[PT][C];
+#pragma unroll
+    for (int p = 0; p < PT; ++p) {
+      const int pr = p * T + t;
+#pragma unroll
+      for (int c = 0; c < C; ++c) z[p][c] = rbuf[c * (M / C) * W + pr];
+    }
+#pragma unroll
+    for (int p = 0; p < PT; ++p) {
+      const int pr = p * T + t;
+      const int k = rank * (M / C) + pr / W;
+      cluster_twiddles<C, Ops::DIR, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);   // w_N^{c k}
+      dft<C, Ops::DIR>(z[p]);                                          // z[q] = X[k + M q]
+    }
+    consume(z, misc + 40);
+    cl_arrive();                                   // rbuf (and, RESID, last panel's xbuf) consumed
+    if constexpr (RES) {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+#pragma unroll
+        for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
+        const int pr = p * T + t;
+        const int k = rank * (M / C) + pr / W;
+        dft<C, -1>(z[p]);                                              // forward DIF first stage
+        cluster_twiddles<C, -1, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);     // w_N^{-q k}
+      }
+      cl_wait();                                   // peers are done with their scatter buffers
+      cl_arrive();                                 // (pairs with the next panel's push wait)
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const int pr = p * T + t;
+        const int w = pr % W, k = rank * (M / C) + pr / W;
+        const uint32_t xo = smem_u32(xbuf + k * W + w), xb = smem_u32(xfull);
+#pragma unroll
+        for (int q = 0; q < C; ++q) st_async_cluster(mapa(xo, (uint32_t)q), z[p][q], mapa(xb, (uint32_t)q));
+      }
+      mbar_wait_cta(xfull, (uint32_t)(it & 1));    // all C peers' scatters landed here
+      if (t == 0) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
+      auto st = [&](int w, int j, float2* x) {
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int row = rank + C * (j + r * (M / RL));
+          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
+        }
+      };
+      En::template run_from_smem<-1>(xbuf, st, tw);
+    } else {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const int pr = p * T + t;
+        const int w = pr % W, k = rank * (M / C) + pr / W;
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          const int row = k + M * q;
+          Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
+        }
+      }
+    }
+    if constexpr (MODE == AZ_TAIL) {              // flush this panel's candidates
+      if (a.rule == RULE_K) {
+        __syncthreads();
+        const uint32_t nc = min(tc.scount[0], (uint32_t)Cf::CAND_SMEM);
+        if (t == 0) misc[32] = nc ? atomicAdd(&a.st->cand_count, nc) : 0u;
+        __syncthreads();
+        const uint32_t b0 = misc[32];
+        for (uint32_t i = t; i < nc; i += T) {
+          const uint32_t g = b0 + i;
+          if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else a.st->cand_overflow = 1u;
+        }
+        __syncthreads();
+        if (t == 0) tc.scount[0] = 0u;
+      }
+    }
+  }
+
+  if (it > 0) cl_wait();                           // pairs with the last arrive
+  if constexpr (MODE == AZ_RESID) {
+    float v = racc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((t & 31) == 0) reinterpret_cast<float*>(misc)[t >> 5] = v;
+    __syncthreads();
+    if (t < 32) {
+      float u = (t < T / 32) ? reinterpret_cast<float*>(misc)[t] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+      if (t == 0) atomicAdd(&a.st->resid2, (double)u);
+    }
+  }
+  if constexpr (MODE == AZ_TAIL) {
+    __syncthreads();
+    if (a.rule == RULE_K) {
+      for (int i = t; i < HIST_BINS; i += T) {
+        const uint32_t c = tc.shist[i];
+        if (c) atomicAdd(&a.hist[i], c);
+      }
+    } else if (t == 0 && tc.scount[1]) {
+      atomicAdd(&a.st->support_fixed, (unsigned long long)tc.scount[1]);
+    }
+  }
+}
+
+// 3-D tensor map {col, rank, m} over a row-major [N][n_rg] complex64 array: element
+// (col, c, m) = row c + C m; box {W, 1, BM}
+cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int N, int C, int W, int BM);
+int az_max_clusters(const void* kernel, int C, int T, size_t smem);
+void az_log_config(int logn, int mode, int C, int W, int NS, int T, size_t smem, int clusters);
+
+template <int LOGN, int MODE>
+static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
+  using Cf = AzClShape<LOGN, MODE>;
+  auto k = az_cluster_kernel<LOGN, MODE>;
+  const size_t smem = Cf::CL_SMEM;
+  static int max_cl = 0;                 // co-resident clusters (per process; one device)
+  if (max_cl == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (Cf::C > 8) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    max_cl = az_max_clusters((const void*)k, Cf::C, Cf::T, smem);
+    if (max_cl <= 0) return cudaErrorInvalidConfiguration;
+    az_log_config(LOGN, MODE, Cf::C, Cf::W, Cf::NS, Cf::T, smem, max_cl);
+  }
+  CUtensorMap tm;
+  cudaError_t e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM);
+  if (e != cudaSuccess) return e;
+  const int npan = n_rg / Cf::W;
+  const int ncl = npan < max_cl ? npan : max_cl;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * Cf::C));
+  cfg.blockDim = dim3(Cf::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = Cf::C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, a, tm);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 template <int LOGN, int MODE>
 static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
   using Cf = AzShape<LOGN, MODE == AZ_RESID>;
+  if constexpr (Cf::C > 1) {
+    return az_cluster_launch<LOGN, MODE>(n_rg, a, s);
+  } else {
   auto k = az_kernel<LOGN, MODE>;
   const size_t smem = (MODE == AZ_TAIL) ? Cf::SMEM_TAIL : (MODE == AZ_RESID) ? Cf::SMEM_RESID : Cf::SMEM_FFT;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -376,6 +669,7 @@ static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
   e = cudaLaunchKernelEx(&cfg, k, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+  }
 }
 
 template <int LOGN, bool R>
