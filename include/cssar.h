@@ -129,7 +129,9 @@ const char* cssar_error_string(int code);
 
 /* ---- test hooks (parity of single sweeps / the select; not needed by users) ---------- */
 /* One range sweep in place on a (Doppler, range-time) array: gbody=1 -> Phi3* F Phi2* F^-1
- * Phi1* (G body), gbody=0 -> Phi1 F Phi2 F^-1 Phi3 (M body). */
+ * Phi1* (G body), gbody=0 -> Phi1 F Phi2 F^-1 Phi3 (M body), with UNNORMALISED transforms:
+ * the result is n_rg times the unitary chain (the operator chain folds the 1/n_rg into the
+ * preceding azimuth sweep's output scale). */
 int cssar_debug_range_sweep(cssar_plan plan, void* U, int gbody, void* stream);
 /* Unitary azimuth DFT of every column: dir = -1 forward, +1 inverse.  in/out may alias. */
 int cssar_debug_az_fft(cssar_plan plan, const void* in, void* out, int dir, void* stream);

@@ -147,10 +147,11 @@ int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yo
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+  a.oscale = (float)(1.0 / (std::sqrt((double)pl->p.n_az) * (double)pl->p.n_rg));
   a.in = (const float2*)X;
   a.out = (float2*)Yout;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_PLAIN, a.n_rg, a, s));
-  RgArgs r{(float2*)Yout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
+  RgArgs r{(float2*)Yout, pl->d_coef, 0, pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Yout;
   a.mask = mask;
@@ -164,11 +165,12 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+  a.oscale = (float)(1.0 / (std::sqrt((double)pl->p.n_az) * (double)pl->p.n_rg));
   a.in = (const float2*)R;
   a.out = (float2*)Xout;
   a.mask = mask;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_MASK, a.n_rg, a, s));
-  RgArgs r{(float2*)Xout, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
+  RgArgs r{(float2*)Xout, pl->d_coef, 0, pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Xout;
   a.mask = nullptr;
@@ -185,6 +187,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+  a.oscale = (float)(1.0 / (std::sqrt((double)pl->p.n_az) * (double)pl->p.n_rg));
   a.thr = prm.thr;
   a.rule = prm.rule;
   a.mu = (float)prm.mu;
@@ -195,7 +198,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.Y = (const float2*)Y;
   a.mask = mask;
   float2* b = (float2*)X;
-  RgArgs r{pl->U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
+  RgArgs r{pl->U, pl->d_coef, 0, pl->d_rg_tab};
   MARK(0);
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
   a.in = b;
@@ -436,7 +439,7 @@ int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, i
 int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
-  RgArgs r{(float2*)U, pl->d_coef, 0, (float)(1.0 / (double)pl->p.n_rg), pl->d_rg_tab};
+  RgArgs r{(float2*)U, pl->d_coef, 0, pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody != 0, (int)pl->p.n_az, r, (cudaStream_t)stream));
   return CSSAR_OK;
 }
@@ -449,6 +452,7 @@ int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* 
   a.n_rg = (int)pl->p.n_rg;
   a.mask_words = (int)(pl->p.n_rg / 32);
   a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+  a.oscale = a.scale;   // plain unitary transform (no range sweep follows)
   a.in = (const float2*)in;
   a.out = (float2*)out;
   CUDA_TRY(launch_az(pl->log_naz, dir < 0 ? AZ_FWD_PLAIN : AZ_INV_PLAIN, a.n_rg, a, (cudaStream_t)stream));

@@ -111,7 +111,7 @@ struct AzOps {
   }
 
   CSSAR_DEV static void epi(const AzArgs& a, size_t idx, float2 x, const Aux& ax, TailCtx& tc) {
-    float2 v = x * a.scale;
+    float2 v = x * (DIR < 0 ? a.oscale : a.scale);        // forward outputs feed a range sweep
     if constexpr (MODE == AZ_INV_MASK) {
       if (!ax.m) v = make_float2(0.f, 0.f);
     }
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 #pragma unroll
         for (int r = 0; r < R0; ++r) {
           const int row = j + r * (M / R0);
-          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
+          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.oscale;
         }
       };
       En::template conv<+1>(s, ld, mid, st, tw);
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = rank + C * (j + r * (M / RL));
-          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.scale;
+          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.oscale;
         }
       };
       En::template run_from_smem<-1>(xbuf, st, tw);

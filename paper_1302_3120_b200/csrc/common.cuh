@@ -151,16 +151,24 @@ CSSAR_DEV uint64_t quad_eval(const Quad& q, int32_t u) {
   return q.c2 * u2 + q.c1 * uu + q.c0;
 }
 
-// exp(+-2 pi i P / 2^64): top 24 bits rounded to nearest, table + polynomial
+// exp(+-2 pi i P / 2^64).  Default: the top 32 bits of P as a signed fraction of a cycle
+// (|f| <= 1/2, i.e. |angle| <= pi, the SFU's most accurate range) through the SFU sin/cos
+// (sin.approx / cos.approx: absolute error ~5e-7; 5 issue slots).  CSSAR_PHASE_TABLE: the
+// earlier exact path, top 24 bits rounded -> 256-entry SMEM table x 2-term polynomial
+// (error < 2e-8, ~13 issue slots + a table load).
 template <bool CONJ>
 CSSAR_DEV float2 phase_from_fixed(const float2* tab256, uint64_t P) {
+#if defined(CSSAR_PHASE_TABLE)
   const uint32_t t = (uint32_t)((P + (1ull << 39)) >> 40) & 0xFFFFFFu;
-#if defined(CSSAR_PHASE_SINCOSPIF)
-  float s, c;
-  sincospif((float)t * (1.0f / 8388608.0f), &s, &c);
-  const float2 e = make_float2(c, s);
-#else
   const float2 e = expi24(tab256, t);
+#else
+  (void)tab256;
+  const int32_t hi = (int32_t)(uint32_t)(P >> 32);
+  const float ang = (float)hi * 1.4629180792671596e-09f;          // 2 pi / 2^32
+  float sn, cs;
+  asm("sin.approx.f32 %0, %1;" : "=f"(sn) : "f"(ang));
+  asm("cos.approx.f32 %0, %1;" : "=f"(cs) : "f"(ang));
+  const float2 e = make_float2(cs, sn);
 #endif
   return make_float2(e.x, CONJ ? -e.y : e.y);
 }

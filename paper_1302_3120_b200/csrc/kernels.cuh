@@ -60,6 +60,7 @@ struct AzArgs {
   int rule;
   float mu;
   float scale;              // 1/sqrt(n_az)
+  float oscale;             // factor on outputs that feed a range sweep: scale/n_rg (range IFFT norm folded in)
   const float2* tw;         // precomputed inter-pass twiddle tables of the az engine (global)
 };
 
@@ -67,7 +68,6 @@ struct RgArgs {
   float2* data;
   const RowCoef* coef;
   int row_base;             // global Doppler row of data row 0
-  float scale;              // 1/n_rg
   const float2* tab;        // [exp(2 pi i h/256), h < 256 | inter-pass twiddle tables] (global)
 };
 

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     float2* dst = data + (size_t)(row0 + b) * N;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r] * a.scale;
+    for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });
 }
 
