@@ -45,7 +45,7 @@ enum {
   CSSAR_ERR_NONFINITE = -6,        /* NaN/Inf reached the iterate (reported when the log is read) */
   CSSAR_ERR_CUDA = -7,             /* a CUDA runtime call failed */
   CSSAR_ERR_WORKSPACE = -8,        /* no / too small workspace bound for cssar_ita_iterate */
-  CSSAR_ERR_NCCL = -9,             /* reserved for the multi-GPU path */
+  CSSAR_ERR_NCCL = -9,             /* NCCL missing or a NCCL call failed (world > 1) */
   CSSAR_ERR_BAD_PLAN = -10         /* NULL plan or world/rank combination not supported */
 };
 
@@ -90,15 +90,31 @@ typedef struct {
 typedef struct cssar_plan_s* cssar_plan;
 
 /* Validate p, build the per-Doppler-bin CSA phase coefficient table (u64 fixed-point
- * cycles) and upload it.  world/rank: 1/0 (single GPU;
- * other values -> CSSAR_ERR_BAD_PLAN in this build).  nccl_unique_id: NULL.
- * Allocates only small device tables (< 4 MB). Synchronous. */
+ * cycles) and upload it.  Allocates only small device tables
+ * (< 4 MB).  Synchronous.
+ *   world == 1 (rank 0, nccl_unique_id NULL): single GPU; every call takes whole arrays.
+ *   world > 1 (<= 16): multi-GPU slab partition (north star "slab-
+ *     partitioned by azimuth lines"): this process is `rank` and owns the row slab of
+ *     n_az/world consecutive azimuth lines [rank*n_az/world, (rank+1)*n_az/world) of Y,
+ *     the mask and X (row-major [n_az/world][n_rg], mask n_rg/32 words per line).
+ *     nccl_unique_id: host pointer to the 128-byte ncclUniqueId from cssar_nccl_unique_id()
+ *     on one rank, distributed by the caller; the plan creates its own NCCL communicator
+ *     (collective call: every rank must call it; NCCL from the process's libnccl.so.2).
+ *     world must divide n_az and n_rg with n_rg/world >= 128 and n_az/world a multiple of
+ *     the range kernel's rows per CTA; else CSSAR_ERR_UNSUPPORTED_SIZE.  Only
+ *     cssar_ita_iterate (the hot path) runs on world > 1 plans; the single-array operator
+ *     calls and debug hooks return CSSAR_ERR_BAD_PLAN.  NCCL failures: CSSAR_ERR_NCCL. */
 int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int rank,
                       const void* nccl_unique_id, void* stream);
 int cssar_plan_destroy(cssar_plan plan);
 
-/* Bytes of device workspace cssar_ita_iterate needs (one complex64 array of the scene
- * size plus a candidate buffer for the exact top-k select, ~8.5 B/sample). */
+/* Fill id_out (host, 128 bytes) with a fresh ncclUniqueId for cssar_plan_create(world > 1). */
+int cssar_nccl_unique_id(void* id_out);
+
+/* Bytes of device workspace cssar_ita_iterate needs: world 1: one complex64 array of the
+ * scene size plus a candidate buffer for the exact top-k select (~8.5 B/sample); world > 1:
+ * four complex64 column-slab arrays (transposes, Y, state), the column-slab mask and the
+ * candidate buffer (~32.6 B per local sample). */
 int cssar_workspace_size(cssar_plan plan, size_t* bytes);
 /* Bind caller-owned workspace (device, 256-byte aligned).  Kept until rebound or the
  * plan is destroyed; the caller keeps it alive. */
@@ -116,7 +132,13 @@ int cssar_image(cssar_plan plan, const void* Y, const uint32_t* mask_bits, void*
  * bound workspace.  log_host (host array of >= iters entries) may be NULL; when given,
  * the call copies the log back and SYNCHRONISES the stream, and reports
  * CSSAR_ERR_NONFINITE if NaN/Inf were seen.  The iteration body is replayed as a CUDA
- * graph captured once per (pointers, params) and cached in the plan. */
+ * graph captured once per (pointers, params) and cached in the plan.
+ * world > 1: Y, mask_bits, X_inout are this rank's row slabs; collective over the ranks
+ * (all must call with the same prm).  Per iteration: 4 NCCL all-to-all transposes between
+ * row slabs (range sweeps) and column slabs (azimuth sweeps), all-reduces of the
+ * residual norm and of the select histograms; the log is global.  PROFILE_STAGES is
+ * ignored.  Results are bitwise identical to world 1 (same kernels, same global indices;
+ * only the floating-point order of the logged residual norm differs). */
 int cssar_ita_iterate(cssar_plan plan, const void* Y, const uint32_t* mask_bits,
                       const cssar_ita_params* prm, void* X_inout, cssar_iter_log* log_host,
                       void* stream);
@@ -126,6 +148,20 @@ int cssar_ita_iterate(cssar_plan plan, const void* Y, const uint32_t* mask_bits,
 int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, int64_t cols, void* stream);
 
 const char* cssar_error_string(int code);
+
+/* ---- single-device emulation of a multi-GPU group (tests of the world > 1 path) ------
+ * A group holds `world` rank plans on the current device and runs exactly the kernels and
+ * schedule of cssar_ita_iterate(world > 1), with the all-to-alls done by device copies
+ * and the all-reduces by a summing kernel, all ranks' work serialised on `stream`.
+ * Y[r], mask_bits[r] (all NULL or none), X_inout[r] are rank r's row slabs. */
+typedef struct cssar_group_s* cssar_group;
+int cssar_group_create(cssar_group* out, const cssar_sar_params* p, int world, void* stream);
+int cssar_group_destroy(cssar_group group);
+int cssar_group_workspace_size(cssar_group group, size_t* bytes_per_rank);
+int cssar_group_bind_workspace(cssar_group group, int rank, void* ws, size_t bytes);
+int cssar_group_ita_iterate(cssar_group group, const void* const* Y, const uint32_t* const* mask_bits,
+                            const cssar_ita_params* prm, void* const* X_inout, cssar_iter_log* log_host,
+                            void* stream);
 
 /* ---- test hooks (parity of single sweeps / the select; not needed by users) ---------- */
 /* One range sweep in place on a (Doppler, range-time) array: gbody=1 -> Phi3* F Phi2* F^-1

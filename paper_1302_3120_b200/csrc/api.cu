@@ -1,7 +1,12 @@
 // libcssar C ABI (include/cssar.h): plan (S0 phase-coefficient table), operator calls and
 // the graph-replayed ITA loop.  Host code only; device work lives in kernels.cu.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -58,6 +63,19 @@ struct cssar_plan_s {
   cudaEvent_t ev[7] = {};
   double stage_ms[6] = {};
   int stage_iters = 0;
+  // ---- multi-GPU slab partition; world == 1 leaves these unset
+  int world = 1, rank = 0;
+  long long nrow = 0, ncol = 0;     // row slab: nrow = n_az/world lines; column slab: ncol = n_rg/world gates
+  int transport = 0;                // kTransportNone / kTransportNccl / kTransportGroup
+  ncclComm_t comm = nullptr;
+  uint32_t* d_lvl = nullptr;        // 1024 level counts of the split fine select
+  // workspace views (world > 1): column slabs [n_az][ncol], blocked row slab [world][nrow][ncol]
+  float2* Ucol = nullptr;
+  float2* Vrow = nullptr;
+  float2* Ycol = nullptr;
+  float2* bcol = nullptr;
+  uint32_t* mcol = nullptr;         // mask bits of the column slab, ncol/32 words per line
+  bool have_mask = false;
 };
 
 namespace {
@@ -139,6 +157,60 @@ int validate_params(const cssar_sar_params& p) {
       std::fprintf(stderr, "libcssar: %s failed: %s\n", #x, cudaGetErrorString(_e)); \
       return CSSAR_ERR_CUDA;                          \
     }                                                 \
+  } while (0)
+
+constexpr int kTransportNone = 0, kTransportNccl = 1, kTransportGroup = 2;
+
+// NCCL entry points resolved at run time from the process's libnccl.so.2 (the one torch
+// loaded, or CSSAR_NCCL_LIB); the single-GPU path never touches NCCL.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+};
+
+NcclApi load_nccl() {
+  NcclApi a;
+  const char* path = std::getenv("CSSAR_NCCL_LIB");
+  void* h = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    std::fprintf(stderr, "libcssar: cannot load NCCL (%s)\n", dlerror());
+    return a;
+  }
+#define NCCL_SYM(f, name) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, name))
+  NCCL_SYM(getUniqueId, "ncclGetUniqueId");
+  NCCL_SYM(commInitRank, "ncclCommInitRank");
+  NCCL_SYM(commDestroy, "ncclCommDestroy");
+  NCCL_SYM(groupStart, "ncclGroupStart");
+  NCCL_SYM(groupEnd, "ncclGroupEnd");
+  NCCL_SYM(send, "ncclSend");
+  NCCL_SYM(recv, "ncclRecv");
+  NCCL_SYM(allReduce, "ncclAllReduce");
+#undef NCCL_SYM
+  a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv &&
+         a.allReduce;
+  return a;
+}
+
+NcclApi& nccl() {
+  static NcclApi a = load_nccl();
+  return a;
+}
+
+#define NCCL_TRY(x)                                                                      \
+  do {                                                                                   \
+    ncclResult_t _r = (x);                                                               \
+    if (_r != ncclSuccess) {                                                             \
+      std::fprintf(stderr, "libcssar: %s failed: NCCL error %d\n", #x, (int)_r);         \
+      return CSSAR_ERR_NCCL;                                                             \
+    }                                                                                    \
   } while (0)
 
 int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yout, cudaStream_t s) {
@@ -236,6 +308,290 @@ double fixed_sigma(const cssar_ita_params& prm) {
   return std::cbrt(54.0) / 4.0 * std::pow(lm, 2.0 / 3.0);
 }
 
+
+// ---------------------------------------------------------------- multi-rank path (world > 1)
+// each rank owns the row slab of n_az/world azimuth lines (the user's arrays).
+// Range sweeps run on row slabs, azimuth sweeps on column slabs of n_rg/world gates; four
+// all-to-all transposes per iteration move between them, and the k-rule select reduces its
+// histograms across ranks.  Block algebra: a column slab [n_az][ncol] is, read as send
+// buffer, the blocks [q][nrow][ncol] for destination q; what rank q receives is the blocked
+// row slab [p][nrow][ncol] the range kernel reads with RgArgs::blk (and vice versa), so no
+// pack/unpack pass is needed inside the loop.  The same schedule drives either one NCCL rank
+// (np == 1) or all ranks of a single-device emulation group (np == world, exchanges done
+// with device copies and a summing kernel) — the group runs the identical kernels.
+struct Ranks {
+  cssar_plan* pl;
+  int np;
+  bool group() const { return pl[0]->transport == kTransportGroup; }
+};
+
+int xchg_a2a(const Ranks& R, void* const* send, void* const* recv, size_t blk, cudaStream_t s) {
+  const int P = R.pl[0]->world;
+  if (R.group()) {
+    for (int p = 0; p < P; ++p)
+      for (int q = 0; q < P; ++q)
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv[q]) + (size_t)p * blk,
+                                 static_cast<const char*>(send[p]) + (size_t)q * blk, blk, cudaMemcpyDeviceToDevice,
+                                 s));
+    return CSSAR_OK;
+  }
+  NcclApi& n = nccl();
+  cssar_plan pl = R.pl[0];
+  NCCL_TRY(n.groupStart());
+  for (int q = 0; q < P; ++q) {
+    NCCL_TRY(n.send(static_cast<const char*>(send[0]) + (size_t)q * blk, blk, ncclUint8, q, pl->comm, s));
+    NCCL_TRY(n.recv(static_cast<char*>(recv[0]) + (size_t)q * blk, blk, ncclUint8, q, pl->comm, s));
+  }
+  NCCL_TRY(n.groupEnd());
+  return CSSAR_OK;
+}
+
+// in-place sum over ranks; dtype 0 = u32, 1 = u64, 2 = f64
+int xchg_allreduce(const Ranks& R, void* const* bufs, int dtype, size_t count, cudaStream_t s) {
+  if (R.group()) {
+    CUDA_TRY(launch_group_sum(dtype, bufs, R.pl[0]->world, (long long)count, s));
+    return CSSAR_OK;
+  }
+  const ncclDataType_t t = dtype == 0 ? ncclUint32 : dtype == 1 ? ncclUint64 : ncclFloat64;
+  NCCL_TRY(nccl().allReduce(bufs[0], bufs[0], count, t, ncclSum, R.pl[0]->comm, s));
+  return CSSAR_OK;
+}
+
+template <class F>
+void gather_ptrs(const Ranks& R, void** out, F f) {
+  for (int i = 0; i < R.np; ++i) out[i] = (void*)f(R.pl[i]);
+}
+
+AzArgs az_col_args(cssar_plan pl, const cssar_ita_params& prm) {
+  AzArgs a{};
+  a.tw = pl->d_az_tab;
+  a.n_rg = (int)pl->ncol;
+  a.mask_words = (int)(pl->ncol / 32);
+  a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+  a.oscale = (float)(1.0 / (std::sqrt((double)pl->p.n_az) * (double)pl->p.n_rg));
+  a.thr = prm.thr;
+  a.rule = prm.rule;
+  a.mu = (float)prm.mu;
+  a.st = pl->d_st;
+  a.hist = pl->d_hist;
+  a.cand = pl->cand;
+  a.cand_cap = pl->cand_cap;
+  a.Y = pl->Ycol;
+  a.mask = pl->have_mask ? pl->mcol : nullptr;
+  a.b = pl->bcol;
+  return a;
+}
+
+RgArgs rg_row_args(cssar_plan pl) {
+  RgArgs r{pl->Vrow, pl->d_coef, (int)(pl->rank * pl->nrow), pl->d_rg_tab, 0, 0};
+  r.log_w = ilog2_exact(pl->ncol);
+  r.blk = pl->nrow * pl->ncol;
+  return r;
+}
+
+// one ITA iteration (S1..S6) of every rank in R
+int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s) {
+  cssar_plan p0 = R.pl[0];
+  const size_t blk = (size_t)p0->nrow * (size_t)p0->ncol * sizeof(float2);
+  void *U[16], *V[16], *B[16];
+  gather_ptrs(R, U, [](cssar_plan q) { return q->Ucol; });
+  gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
+  auto az = [&](int mode) -> int {
+    for (int i = 0; i < R.np; ++i) {
+      cssar_plan pl = R.pl[i];
+      AzArgs a = az_col_args(pl, prm);
+      a.in = mode == AZ_FWD_THR ? pl->bcol : pl->Ucol;
+      a.out = pl->Ucol;
+      if (mode == AZ_RESID) a.tw = pl->d_az_tab_r;
+      CUDA_TRY(launch_az(pl->log_naz, mode, a.n_rg, a, s));
+    }
+    return CSSAR_OK;
+  };
+  auto rg = [&](bool gbody) -> int {
+    for (int i = 0; i < R.np; ++i) {
+      cssar_plan pl = R.pl[i];
+      CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody, (int)pl->nrow, rg_row_args(pl), s));
+    }
+    return CSSAR_OK;
+  };
+  auto local_sel = [&](int part) -> int {
+    for (int i = 0; i < R.np; ++i) {
+      cssar_plan pl = R.pl[i];
+      CUDA_TRY(launch_select_part(part, pl->sm_count, pl->bcol, pl->p.n_az * pl->ncol, prm.k, prm.thr,
+                                  (float)prm.mu, pl->d_st, pl->d_hist, pl->d_hist_full, pl->cand, pl->cand_cap,
+                                  pl->d_lvl, pl->d_log, kLogCap, s));
+    }
+    return CSSAR_OK;
+  };
+#define STEP(x) do { int _rc = (x); if (_rc != CSSAR_OK) return _rc; } while (0)
+  STEP(az(AZ_FWD_THR));                       // S1 on column slabs
+  STEP(xchg_a2a(R, U, V, blk, s));            //    -> blocked row slabs
+  STEP(rg(true));                             // S2
+  STEP(xchg_a2a(R, V, U, blk, s));            //    -> column slabs
+  STEP(az(AZ_RESID));                         // S3
+  STEP(xchg_a2a(R, U, V, blk, s));
+  STEP(rg(false));                            // S4
+  STEP(xchg_a2a(R, V, U, blk, s));
+  STEP(az(AZ_TAIL));                          // S5: local histogram / candidates / support
+  gather_ptrs(R, B, [](cssar_plan q) { return reinterpret_cast<char*>(q->d_st) + offsetof(SelState, resid2); });
+  STEP(xchg_allreduce(R, B, 2, 1, s));
+  if (prm.rule == CSSAR_RULE_KSPARSE) {       // S6: exact (k+1)-th largest over all ranks
+    gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist; });
+    STEP(xchg_allreduce(R, B, 0, HIST_WORDS, s));
+    STEP(local_sel(SEL_COARSE));
+    STEP(local_sel(SEL_FB_HIST));
+    gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist_full; });
+    STEP(xchg_allreduce(R, B, 0, HIST_BINS, s));
+    STEP(local_sel(SEL_FB_PICK));
+    STEP(local_sel(SEL_FINE0_HIST));
+    gather_ptrs(R, B, [](cssar_plan q) { return q->d_lvl; });
+    STEP(xchg_allreduce(R, B, 0, 1024, s));
+    STEP(local_sel(SEL_FINE0_FIND));
+    STEP(xchg_allreduce(R, B, 0, 1024, s));
+    STEP(local_sel(SEL_FINE1_FIND));
+  } else {
+    gather_ptrs(R, B, [](cssar_plan q) {
+      return reinterpret_cast<char*>(q->d_st) + offsetof(SelState, support_fixed);
+    });
+    STEP(xchg_allreduce(R, B, 1, 1, s));
+    for (int i = 0; i < R.np; ++i)
+      CUDA_TRY(launch_lambda_step(R.pl[i]->d_st, prm.thr, (float)prm.mu, R.pl[i]->d_log, kLogCap, s));
+  }
+#undef STEP
+  return CSSAR_OK;
+}
+
+// row slab [nrow][row_elems] (elem bytes each) -> blocks [world][nrow][row_elems/world] in dst
+int pack_rows(cssar_plan pl, const void* src, void* dst, size_t row_elems, size_t elem, cudaStream_t s) {
+  const size_t w = row_elems / (size_t)pl->world;
+  for (int q = 0; q < pl->world; ++q)
+    CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)q * pl->nrow * w * elem, w * elem,
+                               static_cast<const char*>(src) + (size_t)q * w * elem, row_elems * elem, w * elem,
+                               (size_t)pl->nrow, cudaMemcpyDeviceToDevice, s));
+  return CSSAR_OK;
+}
+
+int unpack_rows(cssar_plan pl, const void* src, void* dst, size_t row_elems, size_t elem, cudaStream_t s) {
+  const size_t w = row_elems / (size_t)pl->world;
+  for (int q = 0; q < pl->world; ++q)
+    CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)q * w * elem, row_elems * elem,
+                               static_cast<const char*>(src) + (size_t)q * pl->nrow * w * elem, w * elem, w * elem,
+                               (size_t)pl->nrow, cudaMemcpyDeviceToDevice, s));
+  return CSSAR_OK;
+}
+
+// user row slabs (Y, mask, X_0) -> column slabs Ycol, mcol, bcol
+int setup_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask, void* const* X, cudaStream_t s) {
+  cssar_plan p0 = R.pl[0];
+  const size_t n_rg = (size_t)p0->p.n_rg;
+  const size_t blk = (size_t)p0->nrow * (size_t)p0->ncol * sizeof(float2);
+  void *V[16], *D[16];
+  gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
+  for (int i = 0; i < R.np; ++i) {
+    const int rc = pack_rows(R.pl[i], Y[i], R.pl[i]->Vrow, n_rg, sizeof(float2), s);
+    if (rc != CSSAR_OK) return rc;
+  }
+  gather_ptrs(R, D, [](cssar_plan q) { return q->Ycol; });
+  int rc = xchg_a2a(R, V, D, blk, s);
+  if (rc != CSSAR_OK) return rc;
+  const bool have_mask = mask[0] != nullptr;
+  for (int i = 0; i < R.np; ++i) R.pl[i]->have_mask = have_mask;
+  if (have_mask) {
+    for (int i = 0; i < R.np; ++i) {
+      rc = pack_rows(R.pl[i], mask[i], R.pl[i]->Vrow, n_rg / 32, sizeof(uint32_t), s);
+      if (rc != CSSAR_OK) return rc;
+    }
+    gather_ptrs(R, D, [](cssar_plan q) { return q->mcol; });
+    rc = xchg_a2a(R, V, D, (size_t)p0->nrow * (size_t)(p0->ncol / 32) * sizeof(uint32_t), s);
+    if (rc != CSSAR_OK) return rc;
+  }
+  for (int i = 0; i < R.np; ++i) {
+    rc = pack_rows(R.pl[i], X[i], R.pl[i]->Vrow, n_rg, sizeof(float2), s);
+    if (rc != CSSAR_OK) return rc;
+  }
+  gather_ptrs(R, D, [](cssar_plan q) { return q->bcol; });
+  return xchg_a2a(R, V, D, blk, s);
+}
+
+// X_I = E(b; sigma) on the column slabs, then back to the user row slabs
+int final_multi(const Ranks& R, const cssar_ita_params& prm, void* const* X, cudaStream_t s) {
+  cssar_plan p0 = R.pl[0];
+  const size_t blk = (size_t)p0->nrow * (size_t)p0->ncol * sizeof(float2);
+  void *Bc[16], *V[16];
+  for (int i = 0; i < R.np; ++i)
+    CUDA_TRY(launch_finalize(R.pl[i]->bcol, R.pl[i]->p.n_az * R.pl[i]->ncol, prm.thr, R.pl[i]->d_st, s));
+  gather_ptrs(R, Bc, [](cssar_plan q) { return q->bcol; });
+  gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
+  int rc = xchg_a2a(R, Bc, V, blk, s);
+  if (rc != CSSAR_OK) return rc;
+  for (int i = 0; i < R.np; ++i) {
+    rc = unpack_rows(R.pl[i], R.pl[i]->Vrow, X[i], (size_t)p0->p.n_rg, sizeof(float2), s);
+    if (rc != CSSAR_OK) return rc;
+  }
+  return CSSAR_OK;
+}
+
+int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
+  if (prm->thr != CSSAR_THR_SOFT && prm->thr != CSSAR_THR_HALF) return CSSAR_ERR_INVALID_PARAMS;
+  if (prm->rule != CSSAR_RULE_KSPARSE && prm->rule != CSSAR_RULE_FIXED_LAMBDA) return CSSAR_ERR_INVALID_PARAMS;
+  if (!(prm->mu > 0.0) || !std::isfinite(prm->mu)) return CSSAR_ERR_BAD_MU;
+  if (prm->rule == CSSAR_RULE_KSPARSE && (prm->k < 1 || prm->k >= pl->n)) return CSSAR_ERR_BAD_K;
+  if (prm->rule == CSSAR_RULE_FIXED_LAMBDA && (!(prm->lambda >= 0.0) || !std::isfinite(prm->lambda)))
+    return CSSAR_ERR_BAD_MU;
+  if (prm->iters < 0 || prm->iters > kLogCap) return CSSAR_ERR_INVALID_PARAMS;
+  return CSSAR_OK;
+}
+
+// the whole multi-rank solve for the ranks in R (NCCL rank or emulation group)
+int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask, const cssar_ita_params& prm,
+              void* const* X, cssar_iter_log* log_host, cudaStream_t s, cudaGraphExec_t* gexec, GraphKey* gkey,
+              bool* ghave) {
+  cssar_plan p0 = R.pl[0];
+  const float sigma_fixed = prm.rule == CSSAR_RULE_FIXED_LAMBDA ? (float)fixed_sigma(prm) : 0.f;
+  for (int i = 0; i < R.np; ++i)
+    CUDA_TRY(launch_init_state(R.pl[i]->d_st, R.pl[i]->d_hist, R.pl[i]->d_hist_full, prm.thr, sigma_fixed, s));
+  int rc = setup_multi(R, Y, mask, X, s);
+  if (rc != CSSAR_OK) return rc;
+  if (prm.iters > 0) {
+    GraphKey key{nullptr, (const void*)(uintptr_t)p0->have_mask, nullptr, prm.thr, prm.rule,
+                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu};
+    if (!*ghave || !(*gkey == key)) {
+      if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
+      *ghave = false;
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(p0->cap_stream, cudaStreamCaptureModeThreadLocal));
+      rc = iteration_multi(R, prm, p0->cap_stream);
+      cudaError_t ec = cudaStreamEndCapture(p0->cap_stream, &g);
+      if (rc != CSSAR_OK) { if (g) cudaGraphDestroy(g); return rc; }
+      CUDA_TRY(ec);
+      cudaError_t ei = cudaGraphInstantiate(gexec, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(ei);
+      *gkey = key;
+      *ghave = true;
+    }
+    for (int it = 0; it < prm.iters; ++it) CUDA_TRY(cudaGraphLaunch(*gexec, s));
+  }
+  rc = final_multi(R, prm, X, s);
+  if (rc != CSSAR_OK) return rc;
+  if (log_host) {
+    std::vector<IterLogDev> tmp((size_t)prm.iters);
+    SelState st;
+    if (prm.iters > 0)
+      CUDA_TRY(cudaMemcpyAsync(tmp.data(), p0->d_log, sizeof(IterLogDev) * prm.iters, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&st, p0->d_st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < prm.iters; ++i) {
+      log_host[i].sigma = tmp[i].sigma;
+      log_host[i].lambda = tmp[i].lam;
+      log_host[i].support = tmp[i].support;
+      log_host[i].resid2 = tmp[i].resid2;
+    }
+    if (st.nonfinite) return CSSAR_ERR_NONFINITE;
+  }
+  return CSSAR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -257,20 +613,39 @@ const char* cssar_error_string(int code) {
   }
 }
 
-int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int rank, const void* nccl_unique_id,
-                      void* stream) {
-  (void)nccl_unique_id;
-  (void)stream;
+}  // extern "C"
+
+namespace {
+
+int validate_world(const cssar_sar_params& p, int world, int rank) {
+  if (world < 1 || world > 16 || rank < 0 || rank >= world) return CSSAR_ERR_BAD_PLAN;
+  if (world == 1) return CSSAR_OK;
+  if (p.n_az % world || p.n_rg % world) return CSSAR_ERR_UNSUPPORTED_SIZE;
+  const long long nrow = p.n_az / world, ncol = p.n_rg / world;
+  const int rpc = rg_rows_per_cta(ilog2_exact(p.n_rg));
+  if (ncol < 128 || rpc <= 0 || nrow % rpc) return CSSAR_ERR_UNSUPPORTED_SIZE;
+  return CSSAR_OK;
+}
+
+// plan for one rank; transport kTransportNone (world 1), kTransportNccl or kTransportGroup
+int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int rank, int transport,
+                     const void* nccl_unique_id) {
   if (!out || !p) return CSSAR_ERR_BAD_PLAN;
   *out = nullptr;
-  if (world != 1 || rank != 0) return CSSAR_ERR_BAD_PLAN;
   int v = validate_params(*p);
+  if (v != CSSAR_OK) return v;
+  v = validate_world(*p, world, rank);
   if (v != CSSAR_OK) return v;
   cssar_plan pl = new cssar_plan_s();
   pl->p = *p;
   pl->log_naz = ilog2_exact(p->n_az);
   pl->log_nrg = ilog2_exact(p->n_rg);
   pl->n = p->n_az * p->n_rg;
+  pl->world = world;
+  pl->rank = rank;
+  pl->nrow = p->n_az / world;
+  pl->ncol = p->n_rg / world;
+  pl->transport = transport;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -278,8 +653,9 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
   if (cudaMalloc(&pl->d_coef, sizeof(RowCoef) * tab.size()) != cudaSuccess ||
       cudaMemcpy(pl->d_coef, tab.data(), sizeof(RowCoef) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMalloc(&pl->d_st, sizeof(SelState)) != cudaSuccess ||
-      cudaMalloc(&pl->d_hist, sizeof(uint32_t) * HIST_BINS) != cudaSuccess ||
+      cudaMalloc(&pl->d_hist, sizeof(uint32_t) * HIST_WORDS) != cudaSuccess ||
       cudaMalloc(&pl->d_hist_full, sizeof(uint32_t) * HIST_BINS) != cudaSuccess ||
+      cudaMalloc(&pl->d_lvl, sizeof(uint32_t) * 1024) != cudaSuccess ||
       cudaMalloc(&pl->d_log, sizeof(IterLogDev) * kLogCap) != cudaSuccess ||
       cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&pl->d_rg_tab, sizeof(float2) * rg_table_count(pl->log_nrg)) != cudaSuccess ||
@@ -297,12 +673,82 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
+  if (transport == kTransportNccl) {
+    NcclApi& n = nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (!n.ok || n.commInitRank(&pl->comm, world, id, rank) != ncclSuccess) {
+      pl->comm = nullptr;
+      cssar_plan_destroy(pl);
+      return CSSAR_ERR_NCCL;
+    }
+  }
   *out = pl;
+  return CSSAR_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
+
+// workspace layout: world 1: [U | cand]; world > 1: [Ucol | Vrow | Ycol | bcol | mcol | cand]
+size_t workspace_bytes(cssar_plan pl) {
+  if (pl->world == 1) return sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
+  const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
+  return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + sizeof(uint32_t) * cand_capacity((long long)nl) + 256;
+}
+
+void bind_views(cssar_plan pl, char* ws) {
+  if (pl->world == 1) {
+    pl->U = (float2*)ws;
+    pl->cand = (uint32_t*)(ws + sizeof(float2) * (size_t)pl->n);
+    pl->cand_cap = (uint32_t)cand_capacity(pl->n);
+    return;
+  }
+  const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
+  const size_t a = align256(sizeof(float2) * nl);
+  pl->Ucol = (float2*)ws;
+  pl->Vrow = (float2*)(ws + a);
+  pl->Ycol = (float2*)(ws + 2 * a);
+  pl->bcol = (float2*)(ws + 3 * a);
+  pl->mcol = (uint32_t*)(ws + 4 * a);
+  pl->cand = (uint32_t*)(ws + 4 * a + align256(nl / 8));
+  pl->cand_cap = (uint32_t)cand_capacity((long long)nl);
+  pl->U = pl->Ucol;
+}
+
+}  // namespace
+
+// single-device emulation of a `world`-rank plan group (tests of the multi-GPU schedule)
+struct cssar_group_s {
+  std::vector<cssar_plan> pl;
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  bool ghave = false;
+};
+
+extern "C" {
+
+int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int rank, const void* nccl_unique_id,
+                      void* stream) {
+  (void)stream;
+  if (!out || !p) return CSSAR_ERR_BAD_PLAN;
+  if (world > 1 && !nccl_unique_id) return CSSAR_ERR_BAD_PLAN;
+  return plan_create_impl(out, p, world, rank, world > 1 ? kTransportNccl : kTransportNone, nccl_unique_id);
+}
+
+int cssar_nccl_unique_id(void* id_out) {
+  if (!id_out) return CSSAR_ERR_BAD_PLAN;
+  NcclApi& n = nccl();
+  if (!n.ok) return CSSAR_ERR_NCCL;
+  ncclUniqueId id;
+  NCCL_TRY(n.getUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
   return CSSAR_OK;
 }
 
 int cssar_plan_destroy(cssar_plan pl) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (pl->comm && nccl().ok) nccl().commDestroy(pl->comm);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   for (int i = 0; i < 7; ++i)
@@ -314,44 +760,95 @@ int cssar_plan_destroy(cssar_plan pl) {
   cudaFree(pl->d_st);
   cudaFree(pl->d_hist);
   cudaFree(pl->d_hist_full);
+  cudaFree(pl->d_lvl);
   cudaFree(pl->d_log);
   delete pl;
   return CSSAR_OK;
 }
 
-static size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
-
 int cssar_workspace_size(cssar_plan pl, size_t* bytes) {
   if (!pl || !bytes) return CSSAR_ERR_BAD_PLAN;
-  const size_t u = sizeof(float2) * (size_t)pl->n;
-  *bytes = u + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
+  *bytes = workspace_bytes(pl);
   return CSSAR_OK;
 }
 
 int cssar_bind_workspace(cssar_plan pl, void* ws, size_t bytes) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
-  size_t need = 0;
-  cssar_workspace_size(pl, &need);
-  if (!ws || bytes < need) return CSSAR_ERR_WORKSPACE;
+  if (!ws || bytes < workspace_bytes(pl)) return CSSAR_ERR_WORKSPACE;
   if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return CSSAR_ERR_ALIGNMENT;
   pl->ws = (char*)ws;
   pl->ws_bytes = bytes;
-  pl->U = (float2*)ws;
-  pl->cand = (uint32_t*)((char*)ws + sizeof(float2) * (size_t)pl->n);
-  pl->cand_cap = (uint32_t)cand_capacity(pl->n);
+  bind_views(pl, (char*)ws);
   if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
   pl->ghave = false;
   return CSSAR_OK;
 }
 
+int cssar_group_create(cssar_group* out, const cssar_sar_params* p, int world, void* stream) {
+  (void)stream;
+  if (!out || !p || world < 2) return CSSAR_ERR_BAD_PLAN;
+  *out = nullptr;
+  cssar_group g = new cssar_group_s();
+  for (int r = 0; r < world; ++r) {
+    cssar_plan pl = nullptr;
+    const int rc = plan_create_impl(&pl, p, world, r, kTransportGroup, nullptr);
+    if (rc != CSSAR_OK) {
+      cssar_group_destroy(g);
+      return rc;
+    }
+    g->pl.push_back(pl);
+  }
+  *out = g;
+  return CSSAR_OK;
+}
+
+int cssar_group_destroy(cssar_group g) {
+  if (!g) return CSSAR_ERR_BAD_PLAN;
+  if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  for (cssar_plan pl : g->pl) cssar_plan_destroy(pl);
+  delete g;
+  return CSSAR_OK;
+}
+
+int cssar_group_workspace_size(cssar_group g, size_t* bytes_per_rank) {
+  if (!g || g->pl.empty() || !bytes_per_rank) return CSSAR_ERR_BAD_PLAN;
+  *bytes_per_rank = workspace_bytes(g->pl[0]);
+  return CSSAR_OK;
+}
+
+int cssar_group_bind_workspace(cssar_group g, int rank, void* ws, size_t bytes) {
+  if (!g || rank < 0 || rank >= (int)g->pl.size()) return CSSAR_ERR_BAD_PLAN;
+  if (g->gexec) { cudaGraphExecDestroy(g->gexec); g->gexec = nullptr; }
+  g->ghave = false;
+  return cssar_bind_workspace(g->pl[(size_t)rank], ws, bytes);
+}
+
+int cssar_group_ita_iterate(cssar_group g, const void* const* Y, const uint32_t* const* mask_bits,
+                            const cssar_ita_params* prm, void* const* X_inout, cssar_iter_log* log_host,
+                            void* stream) {
+  if (!g || g->pl.empty() || !prm || !Y || !mask_bits || !X_inout) return CSSAR_ERR_BAD_PLAN;
+  const int P = (int)g->pl.size();
+  for (int r = 0; r < P; ++r) {
+    if (!aligned16(Y[r]) || !aligned16(X_inout[r])) return CSSAR_ERR_ALIGNMENT;
+    if ((mask_bits[r] != nullptr) != (mask_bits[0] != nullptr)) return CSSAR_ERR_INVALID_PARAMS;
+    if (mask_bits[r] && !aligned16(mask_bits[r])) return CSSAR_ERR_ALIGNMENT;
+    if (!g->pl[(size_t)r]->Ucol) return CSSAR_ERR_WORKSPACE;
+  }
+  const int v = validate_ita(g->pl[0], prm);
+  if (v != CSSAR_OK) return v;
+  Ranks R{g->pl.data(), P};
+  return ita_multi(R, Y, mask_bits, *prm, X_inout, log_host, (cudaStream_t)stream, &g->gexec, &g->gkey,
+                   &g->ghave);
+}
+
 int cssar_forward(cssar_plan pl, const void* X, const uint32_t* mask_bits, void* Y_out, void* stream) {
-  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(X) || !aligned16(Y_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
   return enqueue_forward(pl, X, mask_bits, Y_out, (cudaStream_t)stream);
 }
 
 int cssar_adjoint(cssar_plan pl, const void* R, const uint32_t* mask_bits, void* X_out, void* stream) {
-  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(R) || !aligned16(X_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
   return enqueue_adjoint(pl, R, mask_bits, X_out, (cudaStream_t)stream);
 }
@@ -364,15 +861,14 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
                       void* X_inout, cssar_iter_log* log_host, void* stream) {
   if (!pl || !prm) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(Y) || !aligned16(X_inout) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
-  if (prm->thr != CSSAR_THR_SOFT && prm->thr != CSSAR_THR_HALF) return CSSAR_ERR_INVALID_PARAMS;
-  if (prm->rule != CSSAR_RULE_KSPARSE && prm->rule != CSSAR_RULE_FIXED_LAMBDA) return CSSAR_ERR_INVALID_PARAMS;
-  if (!(prm->mu > 0.0) || !std::isfinite(prm->mu)) return CSSAR_ERR_BAD_MU;
-  if (prm->rule == CSSAR_RULE_KSPARSE && (prm->k < 1 || prm->k >= pl->n)) return CSSAR_ERR_BAD_K;
-  if (prm->rule == CSSAR_RULE_FIXED_LAMBDA && (!(prm->lambda >= 0.0) || !std::isfinite(prm->lambda)))
-    return CSSAR_ERR_BAD_MU;
-  if (prm->iters < 0 || prm->iters > kLogCap) return CSSAR_ERR_INVALID_PARAMS;
+  const int v = validate_ita(pl, prm);
+  if (v != CSSAR_OK) return v;
   if (!pl->U) return CSSAR_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pl->world > 1) {                          // this rank's row slabs; NCCL transposes
+    Ranks R{&pl, 1};
+    return ita_multi(R, &Y, &mask_bits, *prm, &X_inout, log_host, s, &pl->gexec, &pl->gkey, &pl->ghave);
+  }
   const float sigma_fixed = prm->rule == CSSAR_RULE_FIXED_LAMBDA ? (float)fixed_sigma(*prm) : 0.f;
   CUDA_TRY(launch_init_state(pl->d_st, pl->d_hist, pl->d_hist_full, prm->thr, sigma_fixed, s));
   const bool prof = (prm->flags & CSSAR_FLAG_PROFILE_STAGES) != 0;
@@ -437,7 +933,7 @@ int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, i
 }
 
 int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
-  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
   RgArgs r{(float2*)U, pl->d_coef, 0, pl->d_rg_tab};
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody != 0, (int)pl->p.n_az, r, (cudaStream_t)stream));
@@ -445,7 +941,7 @@ int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
 }
 
 int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* stream) {
-  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(in) || !aligned16(out)) return CSSAR_ERR_ALIGNMENT;
   AzArgs a{};
   a.tw = pl->d_az_tab;
@@ -461,7 +957,7 @@ int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* 
 
 int cssar_debug_select(cssar_plan pl, const void* b, int64_t k, uint32_t* sigma2_bits_out, int64_t* above_out,
                        void* stream) {
-  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(b)) return CSSAR_ERR_ALIGNMENT;
   if (k < 1 || k >= pl->n) return CSSAR_ERR_BAD_K;
   if (!pl->U) return CSSAR_ERR_WORKSPACE;

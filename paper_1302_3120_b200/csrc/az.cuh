@@ -129,13 +129,13 @@ struct AzOps {
             tc.scand[pos] = u;
           } else {
             const uint32_t g = atomicAdd(&a.st->cand_count, 1u);
-            if (g < a.cand_cap) a.cand[g] = u; else a.st->cand_overflow = 1u;
+            if (g < a.cand_cap) a.cand[g] = u; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
           }
         }
-        if (bin >= (0x7F800000u >> HIST_SHIFT)) a.st->nonfinite = 1u;
+        if (bin >= (0x7F800000u >> HIST_SHIFT)) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
       } else {
         if (u > tc.s2fixed) atomicAdd(&tc.scount[1], 1u);
-        if (u >= 0x7F800000u) a.st->nonfinite = 1u;
+        if (u >= 0x7F800000u) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
       }
     } else {
       a.out[idx] = v;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
       __syncthreads();
       for (uint32_t i = t; i < nc; i += T) {
         const uint32_t g = base + i;
-        if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else a.st->cand_overflow = 1u;
+        if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
       }
     } else if (t == 0 && tc.scount[1]) {
       atomicAdd(&a.st->support_fixed, (unsigned long long)tc.scount[1]);
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         const uint32_t b0 = misc[32];
         for (uint32_t i = t; i < nc; i += T) {
           const uint32_t g = b0 + i;
-          if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else a.st->cand_overflow = 1u;
+          if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
         }
         __syncthreads();
         if (t == 0) tc.scount[0] = 0u;

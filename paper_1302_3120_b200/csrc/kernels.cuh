@@ -18,6 +18,9 @@ enum Rule : int { RULE_K = 1, RULE_LAMBDA = 2 };
 constexpr int HIST_BITS = 11;                  // top bits of the 31-bit |b|^2 pattern
 constexpr int HIST_BINS = 1 << HIST_BITS;      // 2048 bins, 8 per octave of |b|^2
 constexpr int HIST_SHIFT = 31 - HIST_BITS;     // 20
+// the |b|^2 histogram buffer carries two flag words after the bins (summed by the multi-GPU
+// all-reduce together with the bins): [HIST_BINS] candidate overflow, [HIST_BINS+1] non-finite
+constexpr int HIST_WORDS = HIST_BINS + 2;
 constexpr int FLOOR_MARGIN = 8;                // bins below the last sigma^2 bin still counted
 constexpr int CAND_MARGIN = 2;                 // candidate window half-width (bins)
 
@@ -40,6 +43,9 @@ struct SelState {
   double resid2;            // ||Theta(Y - G X)||^2 of the current iteration
   unsigned long long support_fixed;
   int32_t fallbacks;        // # iterations that needed the full-histogram fallback
+  uint32_t fine_prefix;     // split fine select (multi-GPU): matched high bits so far
+  uint32_t fine_rank;       //   rank inside the current prefix
+  unsigned long long fine_abv;  //   elements strictly above the prefix
 };
 
 struct IterLogDev { float sigma; float lam; long long support; double resid2; };
@@ -69,6 +75,11 @@ struct RgArgs {
   const RowCoef* coef;
   int row_base;             // global Doppler row of data row 0
   const float2* tab;        // [exp(2 pi i h/256), h < 256 | inter-pass twiddle tables] (global)
+  // blocked row-slab layout of the multi-GPU path: sample j of local row r lives
+  // at (j >> log_w) * blk + r * 2^log_w + (j & (2^log_w - 1)), i.e. [peer][row][w] blocks as
+  // received from the all-to-all; log_w = log2(n_rg), blk = 0 is the plain row-major layout
+  int log_w;
+  long long blk;
 };
 
 enum AzMode : int {
@@ -82,16 +93,32 @@ enum AzMode : int {
 };
 
 // host-side launchers (kernels.cu)
-cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s);
+cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s);   // blocked iff a.blk != 0
 cudaError_t launch_az(int log_naz, int mode, int n_rg_local, const AzArgs& a, cudaStream_t s);
 cudaError_t launch_select(int n_threads_hint, float2* b, long long n, long long k, int rule, int thr, float mu,
                           SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand, uint32_t cand_cap,
                           IterLogDev* log, int log_cap, cudaStream_t s);
+// multi-GPU k-rule select, split around the all-reduces; world == 1 uses launch_select
+enum SelPart : int {
+  SEL_COARSE = 0,     // global |b|^2 histogram (+ flags) -> target bin or fallback decision
+  SEL_FB_HIST = 1,    // (fallback only) local full histogram -> hist_full
+  SEL_FB_PICK = 2,    // (fallback only) target bin from the global hist_full, collect candidates
+  SEL_FINE0_HIST = 3, // local 1024-bin histogram of the candidates, bits [19:10]
+  SEL_FINE0_FIND = 4, // global level-0 counts -> prefix; then local level-1 histogram, bits [9:0]
+  SEL_FINE1_FIND = 5, // global level-1 counts -> sigma^2, log entry, next window
+};
+cudaError_t launch_select_part(int part, int sm_count, float2* b, long long n, long long k, int thr, float mu,
+                               SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand,
+                               uint32_t cand_cap, uint32_t* lvl, IterLogDev* log, int log_cap, cudaStream_t s);
+cudaError_t launch_lambda_step(SelState* st, int thr, float mu, IterLogDev* log, int log_cap, cudaStream_t s);
+// bufs[p][i] <- sum_p bufs[p][i] for every p (single-device emulation of an all-reduce)
+cudaError_t launch_group_sum(int dtype, void* const* bufs, int world, long long count, cudaStream_t s);
 cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,
                               cudaStream_t s);
 cudaError_t launch_finalize(float2* b, long long n, int thr, const SelState* st, cudaStream_t s);
 // precomputed SMEM tables (filled once per plan, copied into SMEM by each CTA)
 size_t rg_table_count(int log_nrg);
+int rg_rows_per_cta(int log_nrg);
 cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s);
 size_t az_table_count(int log_naz, bool resid);
 cudaError_t az_table_fill(int log_naz, bool resid, float2* dst, cudaStream_t s);

@@ -22,7 +22,7 @@ struct RgCfg {
 
 // GBODY: Phi3* -> F -> Phi2* -> F^-1 -> Phi1*  (inverse of the focusing steps)
 // else : Phi1  -> F -> Phi2  -> F^-1 -> Phi3   (CSA focusing body)
-template <int LOGN, bool GBODY>
+template <int LOGN, bool GBODY, bool BLK>
 __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_kernel(const RgArgs a) {
   using C = RgCfg<LOGN>;
   using En = typename C::En;
@@ -40,10 +40,18 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   constexpr int LR0 = En::template lr<false>(0), LRL = En::template lr<false>(En::P - 1);
 
   float2 v[En::E];
+  // element j of local row rr: plain row-major, or [peer][row][w] blocks (multi-GPU)
+  auto at = [&](int rr, int j) -> size_t {
+    if constexpr (BLK) {
+      const int wm = (1 << a.log_w) - 1;
+      return (size_t)(j >> a.log_w) * (size_t)a.blk + ((size_t)rr << a.log_w) + (size_t)(j & wm);
+    } else {
+      return (size_t)rr * N + j;
+    }
+  };
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // raw row loads
-    const float2* src = data + (size_t)(row0 + b) * N;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) x[r] = src[j + r * (N / R0)];
+    for (int r = 0; r < R0; ++r) x[r] = data[at(row0 + b, j + r * (N / R0))];
   });
   cp_async_wait_all();
   __syncthreads();                                                        // tables visible
@@ -62,9 +70,8 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
     phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
-    float2* dst = data + (size_t)(row0 + b) * N;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) dst[j + r * (N / R0)] = x[r];   // 1/n_rg folded into AzArgs::oscale
+    for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });
 }
 
@@ -73,6 +80,15 @@ __global__ void rg_table_kernel(float2* dst) {
   using C = RgCfg<LOGN>;
   init_expi_table(dst, threadIdx.x, blockDim.x);
   C::En::build_tw(dst + 256, threadIdx.x, blockDim.x);
+}
+
+int rg_rows_per_cta(int log_nrg) {
+  switch (log_nrg) {
+#define RGB(L) case L: return RgCfg<L>::B;
+    RGB(7) RGB(8) RGB(9) RGB(10) RGB(11) RGB(12) RGB(13) RGB(14)
+#undef RGB
+    default: return 0;
+  }
 }
 
 size_t rg_table_count(int log_nrg) {
@@ -93,10 +109,10 @@ cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s) {
   }
 }
 
-template <int LOGN, bool GB>
+template <int LOGN, bool GB, bool BLK>
 static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
   using C = RgCfg<LOGN>;
-  auto k = rg_sweep_kernel<LOGN, GB>;
+  auto k = rg_sweep_kernel<LOGN, GB, BLK>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
   k<<<n_rows / C::B, C::T, C::SMEM, s>>>(a);
@@ -104,7 +120,10 @@ static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s) {
-#define RG_CASE(L) case L: return gbody ? rg_launch<L, true>(n_rows, a, s) : rg_launch<L, false>(n_rows, a, s);
+#define RG_CASE(L)                                                                        \
+  case L:                                                                                 \
+    if (a.blk) return gbody ? rg_launch<L, true, true>(n_rows, a, s) : rg_launch<L, false, true>(n_rows, a, s); \
+    return gbody ? rg_launch<L, true, false>(n_rows, a, s) : rg_launch<L, false, false>(n_rows, a, s);
   switch (log_nrg) {
     RG_CASE(7) RG_CASE(8) RG_CASE(9) RG_CASE(10) RG_CASE(11) RG_CASE(12) RG_CASE(13) RG_CASE(14)
     default: return cudaErrorInvalidValue;

@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(1024) sel_coarse_kernel(long long k, SelState*
     if (above[(0x7F800000u >> HIST_SHIFT)] + cnt[(0x7F800000u >> HIST_SHIFT)] > 0 ||
         cnt[HIST_BINS - 1] > 0)
       st->nonfinite = 1u;
-    const bool ok = sb >= 0 && sb >= st->cand_lo && sb <= st->cand_hi && st->cand_overflow == 0u;
+    if (hist[HIST_BINS + 1]) st->nonfinite = 1u;          // any rank saw NaN/Inf (multi-GPU sum)
+    const bool ok = sb >= 0 && sb >= st->cand_lo && sb <= st->cand_hi && hist[HIST_BINS] == 0u;
     if (ok) {
       st->need_full = 0;
       st->target_bin = sb;
@@ -201,44 +202,12 @@ __global__ void __launch_bounds__(512) fb_collect_kernel(const float2* __restric
   }
 }
 
-// radix refinement inside target_bin over the candidate list, then bookkeeping for the next
-// iteration (new sigma, histogram floor, candidate window, log entry, counter resets)
-__global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, float mu, SelState* st,
-                                                        uint32_t* hist, uint32_t* hist_full, const uint32_t* cand,
-                                                        uint32_t cap, IterLogDev* log, int log_cap) {
-  __shared__ uint32_t cnt[1024], above[1024], wt[32];
-  __shared__ int sd;
-  __shared__ uint32_t sr, sa;
+// sigma^2 found: state for the next iteration (new sigma, histogram floor, candidate window,
+// log entry, counter resets).  Runs in thread 0 (bookkeeping) and all threads (resets).
+CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float mu, SelState* st, uint32_t* hist,
+                             uint32_t* hist_full, IterLogDev* log, int log_cap) {
   const int t = threadIdx.x;
-  const int B = st->target_bin;
-  const uint32_t r0 = st->target_rank;
-  const uint32_t nc = min(st->cand_count, cap);
-  uint32_t prefix = (uint32_t)B;   // matched high bits so far
-  uint32_t rank = r0;
-  unsigned long long abv = st->above_count;
-  // two 10-bit levels: bits [19:10] then [9:0]
-#pragma unroll 1
-  for (int lvl = 0; lvl < 2; ++lvl) {
-    const int sh = lvl == 0 ? 10 : 0;
-    const int hsh = lvl == 0 ? 20 : 10;
-    cnt[t] = 0u;
-    if (t == 0) { sd = -1; sr = 0; sa = 0; }
-    __syncthreads();
-    for (uint32_t i = t; i < nc; i += 1024) {
-      const uint32_t u = cand[i];
-      if ((u >> hsh) == prefix) atomicAdd(&cnt[(u >> sh) & 1023u], 1u);
-    }
-    __syncthreads();
-    block_suffix<1024>(cnt, above, wt);
-    find_rank_bin<1024>(cnt, above, (unsigned long long)rank, &sd, &sr, &sa);
-    const int d = sd < 0 ? 0 : sd;
-    prefix = (prefix << 10) | (uint32_t)d;
-    rank = sr;
-    abv += sa;
-    __syncthreads();
-  }
   if (t == 0) {
-    const uint32_t s2 = prefix;                      // (k+1)-th largest |b|^2 pattern
     const float sig = sqrtf(__uint_as_float(s2));
     st->sigma2_bits = s2;
     st->sigma = sig;
@@ -251,6 +220,7 @@ __global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, fl
       e.resid2 = st->resid2;
       log[it] = e;
     }
+    const int B = (int)(s2 >> HIST_SHIFT);
     st->iter = it + 1;
     st->floor_bin = max(0, B - FLOOR_MARGIN);
     st->cand_lo = B - CAND_MARGIN;
@@ -261,12 +231,99 @@ __global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, fl
   }
   const int nf = st->need_full;
   __syncthreads();
-  for (int i = t; i < HIST_BINS; i += 1024) {
+  for (int i = t; i < HIST_WORDS; i += blockDim.x) {
     hist[i] = 0u;
-    if (nf) hist_full[i] = 0u;
+    if (nf && i < HIST_BINS) hist_full[i] = 0u;
   }
   __syncthreads();
   if (t == 0) st->need_full = 0;
+}
+
+// one 10-bit radix level over the candidates: counts of (u >> sh) & 1023 among u with
+// (u >> (sh + 10)) == prefix
+CSSAR_DEV void fine_count(uint32_t* cnt, const uint32_t* cand, uint32_t nc, uint32_t prefix, int sh) {
+  const int t = threadIdx.x;
+  cnt[t] = 0u;
+  __syncthreads();
+  for (uint32_t i = t; i < nc; i += 1024) {
+    const uint32_t u = cand[i];
+    if ((u >> (sh + 10)) == prefix) atomicAdd(&cnt[(u >> sh) & 1023u], 1u);
+  }
+  __syncthreads();
+}
+
+// radix refinement inside target_bin over the candidate list (two 10-bit levels: bits
+// [19:10] then [9:0]), then finish_select
+__global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, float mu, SelState* st,
+                                                        uint32_t* hist, uint32_t* hist_full, const uint32_t* cand,
+                                                        uint32_t cap, IterLogDev* log, int log_cap) {
+  __shared__ uint32_t cnt[1024], above[1024], wt[32];
+  __shared__ int sd;
+  __shared__ uint32_t sr, sa;
+  const int t = threadIdx.x;
+  const uint32_t nc = min(st->cand_count, cap);
+  uint32_t prefix = (uint32_t)st->target_bin;   // matched high bits so far
+  uint32_t rank = st->target_rank;
+  unsigned long long abv = st->above_count;
+#pragma unroll 1
+  for (int lvl = 0; lvl < 2; ++lvl) {
+    fine_count(cnt, cand, nc, prefix, lvl == 0 ? 10 : 0);
+    if (t == 0) { sd = -1; sr = 0; sa = 0; }
+    __syncthreads();
+    block_suffix<1024>(cnt, above, wt);
+    find_rank_bin<1024>(cnt, above, (unsigned long long)rank, &sd, &sr, &sa);
+    const int d = sd < 0 ? 0 : sd;
+    prefix = (prefix << 10) | (uint32_t)d;
+    rank = sr;
+    abv += sa;
+    __syncthreads();
+  }
+  (void)k;
+  finish_select(prefix, abv, thr, mu, st, hist, hist_full, log, log_cap);
+}
+
+// ---- split fine select (multi-GPU): local level histograms, global counts after the all-reduce
+__global__ void __launch_bounds__(1024) fine_hist_kernel(int lvl, SelState* st, const uint32_t* cand, uint32_t cap,
+                                                         uint32_t* out) {
+  __shared__ uint32_t cnt[1024];
+  if (lvl == 0 && threadIdx.x == 0) {
+    st->fine_prefix = (uint32_t)st->target_bin;
+    st->fine_rank = st->target_rank;
+    st->fine_abv = st->above_count;
+  }
+  __syncthreads();
+  const uint32_t prefix = lvl == 0 ? (uint32_t)st->target_bin : st->fine_prefix;
+  fine_count(cnt, cand, min(st->cand_count, cap), prefix, lvl == 0 ? 10 : 0);
+  out[threadIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(1024) fine_find_kernel(int lvl, int thr, float mu, SelState* st, uint32_t* hist,
+                                                         uint32_t* hist_full, const uint32_t* cand, uint32_t cap,
+                                                         uint32_t* lvl_cnt, IterLogDev* log, int log_cap) {
+  __shared__ uint32_t cnt[1024], above[1024], wt[32];
+  __shared__ int sd;
+  __shared__ uint32_t sr, sa;
+  const int t = threadIdx.x;
+  cnt[t] = lvl_cnt[t];
+  if (t == 0) { sd = -1; sr = 0; sa = 0; }
+  __syncthreads();
+  block_suffix<1024>(cnt, above, wt);
+  find_rank_bin<1024>(cnt, above, (unsigned long long)st->fine_rank, &sd, &sr, &sa);
+  const uint32_t prefix = (st->fine_prefix << 10) | (uint32_t)(sd < 0 ? 0 : sd);
+  const unsigned long long abv = st->fine_abv + sa;
+  __syncthreads();
+  if (lvl == 0) {
+    if (t == 0) {
+      st->fine_prefix = prefix;
+      st->fine_rank = sr;
+      st->fine_abv = abv;
+    }
+    // level-1 local counts for the next all-reduce
+    fine_count(cnt, cand, min(st->cand_count, cap), prefix, 0);
+    lvl_cnt[t] = cnt[t];
+  } else {
+    finish_select(prefix, abv, thr, mu, st, hist, hist_full, log, log_cap);
+  }
 }
 
 __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* log, int log_cap) {
@@ -289,7 +346,7 @@ __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* 
 
 __global__ void init_state_kernel(SelState* st, uint32_t* hist, uint32_t* hist_full, float sigma_fixed) {
   const int t = threadIdx.x;
-  for (int i = t; i < HIST_BINS; i += blockDim.x) { hist[i] = 0u; hist_full[i] = 0u; }
+  for (int i = t; i < HIST_WORDS; i += blockDim.x) { hist[i] = 0u; if (i < HIST_BINS) hist_full[i] = 0u; }
   if (t == 0) {
     SelState z{};
     z.sigma2_bits = 0u;          // X_0 = E(X_in; 0) = X_in (identity threshold)
@@ -341,6 +398,59 @@ cudaError_t launch_select(int sm_count, float2* b, long long n, long long k, int
   fb_find_kernel<<<1, 1024, 0, s>>>(k, st, hist_full);
   fb_collect_kernel<<<grid, 512, 0, s>>>(b, n, st, cand, cand_cap);
   sel_fine_kernel<<<1, 1024, 0, s>>>(k, thr, mu, st, hist, hist_full, cand, cand_cap, log, log_cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_part(int part, int sm_count, float2* b, long long n, long long k, int thr, float mu,
+                               SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand,
+                               uint32_t cand_cap, uint32_t* lvl, IterLogDev* log, int log_cap, cudaStream_t s) {
+  const int grid = sm_count * 4;
+  switch (part) {
+    case SEL_COARSE: sel_coarse_kernel<<<1, 1024, 0, s>>>(k, st, hist); break;
+    case SEL_FB_HIST: fb_hist_kernel<<<grid, 512, 0, s>>>(b, n, st, hist_full); break;
+    case SEL_FB_PICK:
+      fb_find_kernel<<<1, 1024, 0, s>>>(k, st, hist_full);
+      fb_collect_kernel<<<grid, 512, 0, s>>>(b, n, st, cand, cand_cap);
+      break;
+    case SEL_FINE0_HIST: fine_hist_kernel<<<1, 1024, 0, s>>>(0, st, cand, cand_cap, lvl); break;
+    case SEL_FINE0_FIND:
+      fine_find_kernel<<<1, 1024, 0, s>>>(0, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap);
+      break;
+    case SEL_FINE1_FIND:
+      fine_find_kernel<<<1, 1024, 0, s>>>(1, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lambda_step(SelState* st, int thr, float mu, IterLogDev* log, int log_cap, cudaStream_t s) {
+  lambda_step_kernel<<<1, 1, 0, s>>>(st, thr, mu, log, log_cap);
+  return cudaGetLastError();
+}
+
+struct GroupPtrs { void* p[16]; };
+
+template <class T>
+__global__ void group_sum_kernel(GroupPtrs g, int world, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int r = 0; r < world; ++r) acc += static_cast<T*>(g.p[r])[i];
+    for (int r = 0; r < world; ++r) static_cast<T*>(g.p[r])[i] = acc;
+  }
+}
+
+// dtype: 0 = u32, 1 = u64, 2 = f64 (rank order of the sum is fixed: deterministic)
+cudaError_t launch_group_sum(int dtype, void* const* bufs, int world, long long count, cudaStream_t s) {
+  if (world < 1 || world > 16) return cudaErrorInvalidValue;
+  GroupPtrs g{};
+  for (int r = 0; r < world; ++r) g.p[r] = bufs[r];
+  long long blocks = (count + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  if (blocks < 1) blocks = 1;
+  if (dtype == 0) group_sum_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>(g, world, count);
+  else if (dtype == 1) group_sum_kernel<unsigned long long><<<(unsigned)blocks, 256, 0, s>>>(g, world, count);
+  else group_sum_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(g, world, count);
   return cudaGetLastError();
 }
 

@@ -26,7 +26,8 @@ SYMBOLS = [
     "cssar_plan_create", "cssar_plan_destroy", "cssar_workspace_size", "cssar_bind_workspace",
     "cssar_forward", "cssar_adjoint", "cssar_image", "cssar_ita_iterate", "cssar_pack_mask",
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
-    "cssar_debug_fallbacks", "cssar_stage_times",
+    "cssar_debug_fallbacks", "cssar_stage_times", "cssar_nccl_unique_id", "cssar_group_create",
+    "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
@@ -83,6 +84,13 @@ def load_library(path=None):
     lib.cssar_debug_select.argtypes = [P, V, I64, U32P, ctypes.POINTER(ctypes.c_int64), V]
     lib.cssar_debug_fallbacks.argtypes = [P, ctypes.POINTER(ctypes.c_int32), V]
     lib.cssar_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]
+    lib.cssar_nccl_unique_id.argtypes = [V]
+    lib.cssar_group_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SarParamsC), I, V]
+    lib.cssar_group_destroy.argtypes = [P]
+    lib.cssar_group_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
+    lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
+    lib.cssar_group_ita_iterate.argtypes = [P, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(ItaParamsC),
+                                            ctypes.POINTER(V), ctypes.POINTER(IterLogC), V]
     for s in SYMBOLS:
         if s != "cssar_error_string":
             getattr(lib, s).restype = I
@@ -115,6 +123,20 @@ def _params_c(p):
     return SarParamsC(p.fc, p.Kr, p.Tr, p.Fr, p.prf, p.Vr, p.R_ref, p.squint, int(p.n_az), int(p.n_rg))
 
 
+def nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (bytes) for Plan(world > 1)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.cssar_nccl_unique_id(buf), "cssar_nccl_unique_id")
+    return buf.raw
+
+
+def slab_rows(n_az, world, rank):
+    """Azimuth lines [lo, hi) of rank's row slab."""
+    h = int(n_az) // int(world)
+    return rank * h, (rank + 1) * h
+
+
 def pack_mask(mask_u8, stream=None):
     """uint8/bool (n_az, n_rg) device tensor -> bit-packed int32 tensor (n_az, n_rg/32)."""
     lib = load_library()
@@ -128,14 +150,23 @@ def pack_mask(mask_u8, stream=None):
 class Plan:
     """cssar_plan: SAR parameters -> phase-coefficient table; operator calls and ITA."""
 
-    def __init__(self, params, stream=None, workspace=True):
+    def __init__(self, params, stream=None, workspace=True, world=1, rank=0, unique_id=None):
+        """world > 1: this process is `rank` of a slab-partitioned plan; its
+        arrays are row slabs of n_az/world azimuth lines; unique_id = the 128-byte NCCL id
+        (nccl_unique_id() on one rank, shared by the caller, e.g. dist.broadcast_object_list)."""
         self.lib = load_library()
         self.params = params
-        self.shape = (int(params.n_az), int(params.n_rg))
+        self.world, self.rank = int(world), int(rank)
+        self.shape = (int(params.n_az) // self.world, int(params.n_rg))
         h = ctypes.c_void_p()
         pc = _params_c(params)
-        _check(self.lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(pc), 1, 0, None, _stream(stream)),
-               "cssar_plan_create")
+        uid = None
+        if self.world > 1:
+            if unique_id is None or len(unique_id) != 128:
+                raise ValueError("world > 1 needs the 128-byte NCCL unique id")
+            uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(self.lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(pc), self.world, self.rank, uid,
+                                          _stream(stream)), "cssar_plan_create")
         self.h = h
         self.ws = None
         if workspace:
@@ -243,3 +274,61 @@ class Plan:
         v = ctypes.c_int32()
         _check(self.lib.cssar_debug_fallbacks(self.h, ctypes.byref(v), _stream(stream)), "fallbacks")
         return v.value
+
+
+def _itaprm(thr, rule, k, lam, mu, iters, profile_stages=False):
+    return ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
+                      CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
+                      int(k), float(lam), float(mu), int(iters),
+                      CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0)
+
+
+class Group:
+    """cssar_group: `world` rank plans emulated on the current device — the multi-GPU
+    schedule (slab partition, transposes, reduced select) with device-copy exchanges."""
+
+    def __init__(self, params, world, stream=None):
+        self.lib = load_library()
+        self.params = params
+        self.world = int(world)
+        self.shape = (int(params.n_az) // self.world, int(params.n_rg))
+        h = ctypes.c_void_p()
+        pc = _params_c(params)
+        _check(self.lib.cssar_group_create(ctypes.byref(h), ctypes.byref(pc), self.world, _stream(stream)),
+               "cssar_group_create")
+        self.h = h
+        n = ctypes.c_size_t()
+        _check(self.lib.cssar_group_workspace_size(self.h, ctypes.byref(n)), "cssar_group_workspace_size")
+        self.ws = []
+        for r in range(self.world):
+            ws = torch.empty(n.value, dtype=torch.uint8, device="cuda")
+            _check(self.lib.cssar_group_bind_workspace(self.h, r, _ptr(ws), ws.numel()), "cssar_group_bind_workspace")
+            self.ws.append(ws)
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.cssar_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ita_iterate(self, Ys, mask_bits, Xs, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, log=False,
+                    stream=None):
+        """Ys, Xs: lists of row-slab tensors (rank order); mask_bits: list or None."""
+        W = self.world
+        arr = ctypes.c_void_p * W
+        ys = arr(*[_ptr(y) for y in Ys])
+        ms = arr(*([_ptr(m) for m in mask_bits] if mask_bits is not None else [None] * W))
+        xs = arr(*[_ptr(x) for x in Xs])
+        prm = _itaprm(thr, rule, k, lam, mu, iters)
+        logbuf = (IterLogC * max(1, iters))() if log else None
+        _check(self.lib.cssar_group_ita_iterate(self.h, ys, ms, ctypes.byref(prm), xs, logbuf if log else None,
+                                                _stream(stream)), "cssar_group_ita_iterate")
+        if log:
+            return [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2)
+                    for e in list(logbuf)[:iters]]
+        return None

@@ -1,0 +1,105 @@
+"""The multi-GPU slab-partitioned ITA (include/cssar.h world > 1) on one device.
+
+cssar_group runs, for `world` emulated ranks, exactly the kernels and schedule of the NCCL
+path: row slabs of n_az/world azimuth lines for the range sweeps, column slabs of
+n_rg/world gates for the azimuth sweeps, four all-to-all transposes per iteration (device
+copies here, NCCL send/recv on a multi-GPU box) and the select's histograms summed over
+ranks.  Every kernel computes with global indices, so the result must be BITWISE equal to
+the single-GPU plan on the same inputs (only the summation order of the logged residual
+norm differs), and the single-GPU plan is itself pinned to the fp64 oracle
+(test_gpu_ita.py); one case also checks the oracle directly.
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+from oracle import csa, ita
+from tests._common import mask_bits_dev, need_gpu, problem, rel_l2, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def _slabs(a, world):
+    h = a.shape[0] // world
+    return [a[r * h:(r + 1) * h] for r in range(world)]
+
+
+def _group_run(prob, world, iters, rule=None, lam=0.0, masked=True):
+    import torch
+    from paper_1302_3120_b200 import Group
+    cfg = prob.cfg
+    g = Group(cfg.params, world)
+    Ys = [to_dev(y) for y in _slabs(prob.Y, world)]
+    mb = mask_bits_dev(prob.mask)
+    Ms = [m.contiguous() for m in _slabs(mb, world)] if masked else None
+    Xs = [torch.zeros_like(y) for y in Ys]
+    log = g.ita_iterate(Ys, Ms, Xs, thr=cfg.thr, rule=rule or cfg.rule, k=cfg.k, lam=lam, mu=cfg.mu, iters=iters,
+                        log=True)
+    return np.concatenate([to_host(x) for x in Xs], axis=0), log
+
+
+def _single_run(prob, iters, rule=None, lam=0.0, masked=True):
+    from paper_1302_3120_b200 import Plan
+    cfg = prob.cfg
+    pl = Plan(cfg.params)
+    X, log = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask) if masked else None, thr=cfg.thr,
+                            rule=rule or cfg.rule, k=cfg.k, lam=lam, mu=cfg.mu, iters=iters, log=True)
+    return to_host(X), log
+
+
+def _same_logs(la, lb):
+    assert [e["sigma"] for e in la] == [e["sigma"] for e in lb]
+    assert [e["support"] for e in la] == [e["support"] for e in lb]
+    ra = np.array([e["resid2"] for e in la])
+    rb = np.array([e["resid2"] for e in lb])
+    assert np.max(np.abs(ra - rb) / rb) <= 1e-6
+
+
+@pytest.mark.parametrize("name,grid,world,iters", [
+    ("c1", None, 2, 12),            # L1/2 threshold, k = 2%, exact point-target echo
+    ("c1", None, 4, 12),
+    ("c2", (1024, 1024), 8, 8),     # soft, clutter, 30% mask
+    ("c2", None, 16, 4),            # the largest world the library supports
+    ("c3", (2048, 1024), 4, 6),     # line mask
+])
+def test_group_is_bitwise_single_gpu(name, grid, world, iters):
+    prob = problem(name, *(grid or (None, None)))
+    Xs, ls = _single_run(prob, iters)
+    Xg, lg = _group_run(prob, world, iters)
+    assert np.array_equal(Xg.view(np.uint32), Xs.view(np.uint32)), rel_l2(Xg, Xs)
+    _same_logs(lg, ls)
+
+
+def test_group_fixed_lambda_and_no_mask():
+    prob = problem("c2", 512, 512)
+    Xs, ls = _single_run(prob, 5, rule="lambda", lam=0.05, masked=False)
+    Xg, lg = _group_run(prob, 4, 5, rule="lambda", lam=0.05, masked=False)
+    assert np.array_equal(Xg.view(np.uint32), Xs.view(np.uint32)), rel_l2(Xg, Xs)
+    _same_logs(lg, ls)
+
+
+def test_group_matches_oracle_c1():
+    """Independent of the single-GPU path: world 4 vs the fp64 oracle (north-star bar)."""
+    prob = problem("c1", iters=30)
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu,
+                 iters=30)
+    Xg, _ = _group_run(prob, 4, 30)
+    assert rel_l2(Xg, Xo) <= 1e-3
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
+
+
+def test_world_validation():
+    from paper_1302_3120_b200 import Group, CssarError
+    p = configs.get("c0").params            # 128 x 128: n_rg / 2 = 64 < 128 gates per column slab
+    with pytest.raises(CssarError) as e:
+        Group(p, 2)
+    assert e.value.code == -2
+    with pytest.raises(CssarError):
+        Group(configs.get("c1").params, 32)  # world > 16
