@@ -10,7 +10,10 @@ from inputs/ (seeded), echo Y = Theta o (G(X_true) + noise) generated with the l
 own forward operator (P:L47 inverse-focusing simulation); arrays are 512 MiB each, larger
 than L2 (126 MB), so no L2 flush is needed between steps.
 
-Prints ONE JSON line (rank 0).  value = complex samples * iterations / s over all ranks.
+Prints ONE JSON line (rank 0).  value = complex samples * iterations / s of the scene.
+N > 1 (torchrun): the SAME c3 scene slab-partitioned over the ranks by azimuth lines
+(NCCL all-to-all transposes between range and azimuth sweeps, reduced exact
+select) -> "scaling": "strong"; the time is the max over ranks.
 """
 import argparse
 import json
@@ -195,11 +198,22 @@ def main():
     p = cfg.params
     n = p.n_az * p.n_rg
     plan = Plan(p)
-    # weak scaling: each rank reconstructs its own scene (independent seeds) — see DESIGN.md
-    Y, mb, mask, sc = make_problem_gpu(cfg, plan, seed_offset=rank)
+    Y, mb, mask, sc = make_problem_gpu(cfg, plan)
     X = torch.zeros_like(Y)
     kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
-
+    if world > 1:
+        # strong scaling: ONE scene slab-partitioned by azimuth lines; NCCL
+        # all-to-all transposes inside libcssar, communicator from a broadcast unique id
+        from paper_1302_3120_b200 import nccl_unique_id, slab_rows
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        lo, hi = slab_rows(p.n_az, world, rank)
+        Y = Y[lo:hi].contiguous()
+        mb = mb[lo:hi].contiguous()
+        X = torch.zeros_like(Y)
+        del plan
+        torch.cuda.synchronize()
+        plan = Plan(p, world=world, rank=rank, unique_id=uid[0])
     sampler = ClockSampler(local)
     sampler.start()
     plan.ita_iterate(Y, mb, X=X, iters=args.warmup, **kw)
@@ -220,14 +234,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * n * args.steps / (ms * 1e-3)
+    value = n * args.steps / (ms * 1e-3)       # global samples (one scene over all ranks)
     it_s = args.steps / (ms * 1e-3)
     peak, peak_kind = peaks()
 
     # per-step breakdown (CUDA events on the launch stream inside the library)
     stages = None
     roof = None
-    if not args.no_profile:
+    if not args.no_profile and world == 1:
         kp = max(3, min(args.steps, 30))
         plan.ita_iterate(Y, mb, X=X, iters=kp, profile_stages=True, **kw)
         st_ms, it_meas = plan.stage_times()
@@ -247,35 +261,45 @@ def main():
     line = {
         "metric": "ITA complex samples*iterations/s (HBM roofline fraction alongside)",
         "value": value, "unit": "samples*it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "it_per_s": it_s, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_step, "it_per_s": it_s, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {p.n_az}x{p.n_rg} complex64, {cfg.scene} scene, {cfg.mask} mask "
                                f"{cfg.rate}, SNR {cfg.snr_db} dB, {cfg.thr} threshold, k = {cfg.k}, mu = {cfg.mu}",
                    "n_az": p.n_az, "n_rg": p.n_rg, "k": cfg.k, "l2": "inputs larger than L2 (512 MiB arrays)",
-                   "parallelism": "single" if world == 1 else f"replicas{world} (independent scenes per GPU)"},
+                   "parallelism": "single" if world == 1 else
+                   f"slab{world} (azimuth-line row slabs, NCCL all-to-all transposes, reduced select)"},
         "roofline": roof,
-        "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak, "unit": "GB/s",
-                               "frac": iter_ach / peak, "bytes_per_sample": ITER_BYTES_PER_SAMPLE},
+        "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak * world, "unit": "GB/s",
+                               "frac": iter_ach / (peak * world), "bytes_per_sample": ITER_BYTES_PER_SAMPLE,
+                               "note": "aggregate over ranks; excludes NVLink transpose bytes" if world > 1 else None},
         "stages_ms": stages,
-        "gpu_launches": args.steps * (10 if cfg.rule == "k" else 6) + 2,
+        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if world == 1 else (12 if cfg.rule == "k" else 6)) + 2,
         "select_fallbacks": plan.debug_fallbacks(),
         "clocks": clocks,
     }
 
-    if rank == 0 and not args.no_e2e:
+    if not args.no_e2e:
         # end to end through the public API: pinned host Y + mask -> device -> full solve -> host X
+        # (world > 1: every rank its row slabs, collective solve, time = max over ranks)
         Yh = Y.cpu().pin_memory()
         mbh = mb.cpu().pin_memory()
         Xh = torch.empty_like(Yh).pin_memory()
         iters = cfg.iters
         plan.solve_host(Yh, mbh, out_host=Xh, iters=iters, **kw)      # warm (graph capture for new X)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         plan.solve_host(Yh, mbh, out_host=Xh, iters=iters, **kw)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        h2d = Yh.numel() * 8 + mbh.numel() * 4
-        d2h = Xh.numel() * 8
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = (Yh.numel() * 8 + mbh.numel() * 4) * world
+        d2h = Xh.numel() * 8 * world
         line["e2e"] = {"value": n * iters / dt, "unit": "samples*it/s", "h2d_bytes_per_step": h2d / iters,
                        "d2h_bytes_per_step": d2h / iters, "solve_iters": iters,
                        "note": "one full reconstruction (config iteration count) per call; copies once per solve"}
