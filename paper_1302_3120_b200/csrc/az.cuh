@@ -13,10 +13,13 @@ template <int LOGN, bool R>
 struct AzCfg {
   // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
   // C > 1: persistent cluster kernel with NS TMA stages of M*W complex64 per CTA
+  // (measured on c3: head/tail C = 8, W = 4, one stage -> 64 KB SMEM, 2 CTAs/SM, 33 clusters;
+  // residual C = 8, W = 8, one stage + receive + scatter buffers, 1 CTA/SM)
   static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
-  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 10 ? 4 : LOGN <= 14 ? 8 : 4;
+  static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 10 ? 4 : LOGN == 13 ? (R ? 8 : 4)
+                         : LOGN <= 14 ? 8 : 4;
   static constexpr int E = 16;
-  static constexpr int NS = R ? 1 : 2;       // RESID also holds the receive + scatter buffers
+  static constexpr int NS = 1;
 };
 #if defined(CSSAR_AZ13_C)
 template <>
@@ -31,7 +34,7 @@ struct AzCfg<13, true> {
 };
 #endif
 
-template <int LOGN, bool R = false, int NSO = 0>
+template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true>
 struct AzShape {
   using P = AzCfg<LOGN, R>;
   static constexpr int C = P::C, W = P::W, E = P::E, NS = NSO > 0 ? NSO : P::NS;
@@ -56,7 +59,7 @@ struct AzShape {
   static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TW + 15) / 16) * 16;
   static constexpr size_t CL_BAR_OFF = CL_CTW_OFF + sizeof(float2) * CTW;
   static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 16 + 8;
-  static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (HIST_BINS + CAND_SMEM + 4));
+  static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (TAILM ? HIST_BINS + CAND_SMEM + 4 : 0));
   static constexpr int CL_MINB = T <= 256 ? 2 : 1;
 };
 
@@ -348,7 +351,7 @@ CSSAR_DEV void mbar_wait_cta(const uint64_t* bar, uint32_t parity) {
 }
 
 template <int LOGN, int MODE>
-using AzClShape = AzShape<LOGN, MODE == AZ_RESID, MODE == AZ_TAIL ? 1 : 0>;
+using AzClShape = AzShape<LOGN, MODE == AZ_RESID, 0, MODE == AZ_TAIL>;
 
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
