@@ -14,23 +14,27 @@ struct AzCfg {
   // column panel of W range bins, split over a cluster of C CTAs (M = N/C rows each);
   // C > 1: persistent cluster kernel with NS TMA stages of M*W complex64 per CTA
   // (measured on c3: head/tail C = 8, W = 4, one stage -> 64 KB SMEM, 2 CTAs/SM, 33 clusters;
-  // residual C = 8, W = 8, one stage + receive + scatter buffers, 1 CTA/SM)
-  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? 8 : 16;
+  // residual C = 16, W = 8, one stage that also takes the scatter (XS) + receive buffer,
+  // 73 KB, 14 clusters)
+  static constexpr int C = LOGN <= 10 ? 1 : LOGN == 11 ? 2 : LOGN == 12 ? 4 : LOGN == 13 ? (R ? 16 : 8) : 16;
   static constexpr int W = LOGN <= 8 ? 16 : LOGN == 9 ? 8 : LOGN == 10 ? 4 : LOGN == 13 ? (R ? 8 : 4)
                          : LOGN <= 14 ? 8 : 4;
   static constexpr int E = 16;
   static constexpr int NS = 1;
+  static constexpr bool XS = true;           // RESID: scatter into the (one) stage buffer
 };
 #if defined(CSSAR_AZ13_C)
 template <>
 struct AzCfg<13, false> {
   static constexpr int C = CSSAR_AZ13_C, W = CSSAR_AZ13_W, E = CSSAR_AZ13_E, NS = CSSAR_AZ13_NS;
+  static constexpr bool XS = false;
 };
 #endif
 #if defined(CSSAR_AZ13R_C)
 template <>
 struct AzCfg<13, true> {
   static constexpr int C = CSSAR_AZ13R_C, W = CSSAR_AZ13R_W, E = CSSAR_AZ13R_E, NS = CSSAR_AZ13R_NS;
+  static constexpr bool XS = CSSAR_AZ13R_XS;
 };
 #endif
 
@@ -38,6 +42,9 @@ template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true>
 struct AzShape {
   using P = AzCfg<LOGN, R>;
   static constexpr int C = P::C, W = P::W, E = P::E, NS = NSO > 0 ? NSO : P::NS;
+  // RESID with XS: the scatter lands in the stage buffer itself (one stage, refilled after
+  // the panel's last transform) -> no separate scatter buffer, 2 CTAs/SM fit
+  static constexpr bool XS = R && P::XS && NS == 1;
   static constexpr int LOGM = LOGN - ilog2c(C);
   static constexpr int M = 1 << LOGM;
   static constexpr int T = M * W / E;
@@ -53,7 +60,7 @@ struct AzShape {
   // (TAIL) hist, candidates, counters], 1024-byte aligned stages
   static constexpr int BM = M < 256 ? M : 256;             // TMA box rows (box dims <= 256)
   static constexpr uint32_t STAGE_BYTES = (uint32_t)(sizeof(float2) * M * W);
-  static constexpr size_t CL_TW_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R ? 1 : 0));
+  static constexpr size_t CL_TW_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0));
   static constexpr int LO = (LOGN + 1) / 2;                      // cluster twiddle table split
   static constexpr int CTW = (1 << LO) + (1 << (LOGN - LO));      // lo[2^LO] | hi[N / 2^LO]
   static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TW + 15) / 16) * 16;
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   char* base = reinterpret_cast<char*>(smem4) + ((1024u - (smem_u32(smem4) & 1023u)) & 1023u);
   float2* stages = reinterpret_cast<float2*>(base);
   float2* rbuf = stages + (size_t)NS * M * W;                      // pushed partial transforms [c][k][w]
-  float2* xbuf = rbuf + (size_t)M * W;                              // RESID scatter target
+  float2* const xbuf0 = rbuf + (size_t)M * W;                       // RESID scatter target (!XS)
   float2* tw = reinterpret_cast<float2*>(base + Cf::CL_TW_OFF);
   float2* ctw = reinterpret_cast<float2*>(base + Cf::CL_CTW_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cf::CL_BAR_OFF);
@@ -474,10 +481,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     };
     float2 v[E];
     En::template run_keep<Ops::DIR>(s, v, ld, tw);
-    __syncthreads();                               // stage fully read: refill it NS panels ahead
-    if (t == 0 && next < npan) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(next, sidx);
+    float2* const xbuf = Cf::XS ? s : xbuf0;
+    if constexpr (!Cf::XS) {
+      __syncthreads();                             // stage fully read: refill it NS panels ahead
+      if (t == 0 && next < npan) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(next, sidx);
+      }
     }
     // push local output k of every column to its owner rank k / (M/C): rbuf[(rank M/C + k%(M/C)) W + w]
     if (it > 0) cl_wait();                         // owners are done reading their receive buffers
@@ -541,6 +551,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       };
       En::template run_from_smem<-1>(xbuf, st, tw);
+      if constexpr (Cf::XS) {
+        __syncthreads();                           // last transform done with the stage
+        if (t == 0 && next < npan) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(next, sidx);
+        }
+      }
     } else {
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
