@@ -112,12 +112,75 @@ struct AzOps {
     return x;
   }
 
+  // two adjacent columns (col even): one 16-byte load of b, one mask word
+  CSSAR_DEV static void fetch2(const AzArgs& a, int row, int col, size_t idx, Aux& x0, Aux& x1) {
+    x0 = Aux{make_float2(0.f, 0.f), 1u};
+    x1 = x0;
+    if constexpr (MODE == AZ_TAIL) {
+      const float4 q = *reinterpret_cast<const float4*>(a.b + idx);
+      x0.v = make_float2(q.x, q.y);
+      x1.v = make_float2(q.z, q.w);
+    } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_RESID) {
+      const uint32_t wd = a.mask ? __ldg(a.mask + (size_t)row * a.mask_words + (col >> 5)) : 0xFFFFFFFFu;
+      x0.m = (wd >> (col & 31)) & 1u;
+      x1.m = (wd >> ((col + 1) & 31)) & 1u;
+      if constexpr (MODE == AZ_RESID) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(a.Y + idx));
+        x0.v = make_float2(q.x, q.y);
+        x1.v = make_float2(q.z, q.w);
+      }
+    }
+  }
+
   // RESID mid: g = G(X) sample; r = Theta o (Y - g)
   CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc) {
     const float2 g = x * a.scale;
     const float2 r = ax.m ? (ax.v - g) : make_float2(0.f, 0.f);
     acc = fmaf(r.x, r.x, fmaf(r.y, r.y, acc));
     return r;
+  }
+
+  // two adjacent columns: per-element epilogue, one 16-byte store
+  CSSAR_DEV static void epi2(const AzArgs& a, size_t idx, float2 x0, float2 x1, const Aux& a0, const Aux& a1,
+                             TailCtx& tc) {
+    const float sc = DIR < 0 ? a.oscale : a.scale;
+    float2 v0 = x0 * sc, v1 = x1 * sc;
+    if constexpr (MODE == AZ_INV_MASK) {
+      if (!a0.m) v0 = make_float2(0.f, 0.f);
+      if (!a1.m) v1 = make_float2(0.f, 0.f);
+    }
+    if constexpr (MODE == AZ_TAIL) {
+      const float2 k0 = threshold(a0.v, tc.s2bits, tc.sigma, a.thr), k1 = threshold(a1.v, tc.s2bits, tc.sigma, a.thr);
+      v0 = make_float2(fmaf(a.mu, v0.x, k0.x), fmaf(a.mu, v0.y, k0.y));
+      v1 = make_float2(fmaf(a.mu, v1.x, k1.x), fmaf(a.mu, v1.y, k1.y));
+      *reinterpret_cast<float4*>(a.b + idx) = make_float4(v0.x, v0.y, v1.x, v1.y);
+      tail_stats(a, v0, tc);
+      tail_stats(a, v1, tc);
+    } else {
+      *reinterpret_cast<float4*>(a.out + idx) = make_float4(v0.x, v0.y, v1.x, v1.y);
+    }
+  }
+
+  // histogram / candidates / support of one new b (TAIL)
+  CSSAR_DEV static void tail_stats(const AzArgs& a, float2 bn, TailCtx& tc) {
+    const uint32_t u = mag2_bits(bn);
+    const int bin = (int)(u >> HIST_SHIFT);
+    if (a.rule == RULE_K) {
+      if (bin >= tc.floor_bin) atomicAdd(&tc.shist[bin], 1u);
+      if (bin >= tc.cand_lo && bin <= tc.cand_hi) {
+        const uint32_t pos = atomicAdd(&tc.scount[0], 1u);
+        if (pos < 1024u) {
+          tc.scand[pos] = u;
+        } else {
+          const uint32_t g = atomicAdd(&a.st->cand_count, 1u);
+          if (g < a.cand_cap) a.cand[g] = u; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
+        }
+      }
+      if (bin >= (0x7F800000u >> HIST_SHIFT)) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
+    } else {
+      if (u > tc.s2fixed) atomicAdd(&tc.scount[1], 1u);
+      if (u >= 0x7F800000u) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
+    }
   }
 
   CSSAR_DEV static void epi(const AzArgs& a, size_t idx, float2 x, const Aux& ax, TailCtx& tc) {
@@ -129,24 +192,7 @@ struct AzOps {
       const float2 xk = threshold(ax.v, tc.s2bits, tc.sigma, a.thr);     // X_i recomputed
       const float2 bn = make_float2(fmaf(a.mu, v.x, xk.x), fmaf(a.mu, v.y, xk.y));
       a.b[idx] = bn;
-      const uint32_t u = mag2_bits(bn);
-      const int bin = (int)(u >> HIST_SHIFT);
-      if (a.rule == RULE_K) {
-        if (bin >= tc.floor_bin) atomicAdd(&tc.shist[bin], 1u);
-        if (bin >= tc.cand_lo && bin <= tc.cand_hi) {
-          const uint32_t pos = atomicAdd(&tc.scount[0], 1u);
-          if (pos < 1024u) {
-            tc.scand[pos] = u;
-          } else {
-            const uint32_t g = atomicAdd(&a.st->cand_count, 1u);
-            if (g < a.cand_cap) a.cand[g] = u; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
-          }
-        }
-        if (bin >= (0x7F800000u >> HIST_SHIFT)) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
-      } else {
-        if (u > tc.s2fixed) atomicAdd(&tc.scount[1], 1u);
-        if (u >= 0x7F800000u) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
-      }
+      tail_stats(a, bn, tc);
     } else {
       a.out[idx] = v;
     }
@@ -337,6 +383,18 @@ CSSAR_DEV void cluster_twiddles(float2* x, uint32_t k, const float2* ctw) {
   }
 }
 
+template <int C, int DIR, int LOGN, int LO>
+CSSAR_DEV void cluster_twiddles2(float2* x, float2* y, uint32_t k, const float2* ctw) {
+  constexpr uint32_t NM = (1u << LOGN) - 1u, LM = (1u << LO) - 1u;
+#pragma unroll
+  for (int c = 1; c < C; ++c) {
+    const uint32_t m = ((uint32_t)c * k) & NM;
+    const float2 w = cmul(ctw[m & LM], ctw[(1u << LO) + (m >> LO)]);
+    x[c] = DIR < 0 ? cmul(x[c], w) : cmulc(x[c], w);
+    y[c] = DIR < 0 ? cmul(y[c], w) : cmulc(y[c], w);
+  }
+}
+
 // async DSMEM store that signals the destination CTA's mbarrier (same SMEM offset mapped)
 CSSAR_DEV void st_async_cluster(uint32_t raddr, float2 v, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
@@ -391,6 +449,17 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   uint32_t* misc = reinterpret_cast<uint32_t*>(base + Cf::CL_MISC_OFF);   // [0..31] reduce, [32] base
   const int t = threadIdx.x;
   const int rank = (int)cluster_rank();
+  // VEC: a thread's gather slots come in adjacent-column pairs (16-byte loads and stores,
+  // one cluster twiddle set per pair); slot p -> (w, k)
+  constexpr bool VEC = !RES && PT % 2 == 0 && W % 2 == 0;
+  auto slot_w = [&](int p) -> int {
+    if constexpr (VEC) return ((p / 2) * T + threadIdx.x) % (W / 2) * 2 + (p & 1);
+    else return (p * T + threadIdx.x) % W;
+  };
+  auto slot_k = [&](int p) -> int {
+    if constexpr (VEC) return rank * (M / C) + ((p / 2) * T + threadIdx.x) / (W / 2);
+    else return rank * (M / C) + (p * T + threadIdx.x) / W;
+  };
   const int cid = blockIdx.x / C, ncl = gridDim.x / C;
   const int n_rg = a.n_rg;
   const int npan = n_rg / W;
@@ -460,14 +529,25 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     // epilogue / residual inputs of output rows k + M q (in flight during the FFT)
     Aux ax[PT][C];
     if constexpr (AUX) {
+      if constexpr (VEC) {
 #pragma unroll
-      for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
+        for (int p = 0; p < PT; p += 2) {
+          const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
-        for (int q = 0; q < C; ++q) {
-          const int row = k + M * q;
-          ax[p][q] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+          for (int q = 0; q < C; ++q) {
+            const int row = k + M * q;
+            Ops::fetch2(a, row, col0 + w, (size_t)row * n_rg + col0 + w, ax[p][q], ax[p + 1][q]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < PT; ++p) {
+          const int w = slot_w(p), k = slot_k(p);
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const int row = k + M * q;
+            ax[p][q] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
+          }
         }
       }
     }
@@ -506,18 +586,33 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     mbar_wait_cta(rfull, (uint32_t)(it & 1));      // all C partial transforms of our block landed
     if (t == 0) mbar_expect_tx(rfull, Cf::STAGE_BYTES);   // re-arm for the next panel
     float2 z[PT][C];
+    if constexpr (VEC) {
 #pragma unroll
-    for (int p = 0; p < PT; ++p) {
-      const int pr = p * T + t;
+      for (int p = 0; p < PT; p += 2) {
+        const int off = (slot_k(p) - rank * (M / C)) * W + slot_w(p);
 #pragma unroll
-      for (int c = 0; c < C; ++c) z[p][c] = rbuf[c * (M / C) * W + pr];
-    }
+        for (int c = 0; c < C; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(rbuf + c * (M / C) * W + off);
+          z[p][c] = make_float2(q.x, q.y);
+          z[p + 1][c] = make_float2(q.z, q.w);
+        }
+        cluster_twiddles2<C, Ops::DIR, LOGN, Cf::LO>(z[p], z[p + 1], (uint32_t)slot_k(p), ctw);
+        dft<C, Ops::DIR>(z[p]);
+        dft<C, Ops::DIR>(z[p + 1]);
+      }
+    } else {
 #pragma unroll
-    for (int p = 0; p < PT; ++p) {
-      const int pr = p * T + t;
-      const int k = rank * (M / C) + pr / W;
-      cluster_twiddles<C, Ops::DIR, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);   // w_N^{c k}
-      dft<C, Ops::DIR>(z[p]);                                          // z[q] = X[k + M q]
+      for (int p = 0; p < PT; ++p) {
+        const int pr = p * T + t;
+#pragma unroll
+        for (int c = 0; c < C; ++c) z[p][c] = rbuf[c * (M / C) * W + pr];
+      }
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const int k = slot_k(p);
+        cluster_twiddles<C, Ops::DIR, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);   // w_N^{c k}
+        dft<C, Ops::DIR>(z[p]);                                          // z[q] = X[k + M q]
+      }
     }
     consume(z, misc + 40);
     cl_arrive();                                   // rbuf (and, RESID, last panel's xbuf) consumed
@@ -558,11 +653,20 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           issue(next, sidx);
         }
       }
+    } else if constexpr (VEC) {
+#pragma unroll
+      for (int p = 0; p < PT; p += 2) {
+        const int w = slot_w(p), k = slot_k(p);
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          const int row = k + M * q;
+          Ops::epi2(a, (size_t)row * n_rg + col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc);
+        }
+      }
     } else {
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
-        const int pr = p * T + t;
-        const int w = pr % W, k = rank * (M / C) + pr / W;
+        const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
