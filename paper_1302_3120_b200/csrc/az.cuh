@@ -30,6 +30,18 @@ struct AzCfg<13, false> {
   static constexpr bool XS = false;
 };
 #endif
+#if defined(CSSAR_AZ12_C)
+template <>
+struct AzCfg<12, false> {
+  static constexpr int C = CSSAR_AZ12_C, W = CSSAR_AZ12_W, E = CSSAR_AZ12_E, NS = 1;
+  static constexpr bool XS = false;
+};
+template <>
+struct AzCfg<12, true> {
+  static constexpr int C = CSSAR_AZ12_C, W = CSSAR_AZ12_W, E = CSSAR_AZ12_E, NS = 1;
+  static constexpr bool XS = true;
+};
+#endif
 #if defined(CSSAR_AZ13R_C)
 template <>
 struct AzCfg<13, true> {
@@ -51,6 +63,7 @@ struct AzShape {
   static constexpr int MINB = T <= 128 ? 4 : T <= 256 ? (E == 32 ? 2 : 3) : (E == 32 ? 1 : 2);
   using En = Engine<LOGM, W, T, true, E>;
   static constexpr int TW = En::TW_TOTAL;
+  static constexpr int TWK = R ? En::TW_TOTAL : En::TW_FWD;      // SMEM tables of the cluster kernel
   static constexpr int CAND_SMEM = 1024;
   // C == 1 (az_kernel): [twiddles | panel | (TAIL) hist, candidates, counters]
   static constexpr size_t SMEM_FFT = sizeof(float2) * (M * W + TW);
@@ -63,11 +76,11 @@ struct AzShape {
   static constexpr size_t CL_TW_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0));
   static constexpr int LO = (LOGN + 1) / 2;                      // cluster twiddle table split
   static constexpr int CTW = (1 << LO) + (1 << (LOGN - LO));      // lo[2^LO] | hi[N / 2^LO]
-  static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TW + 15) / 16) * 16;
+  static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TWK + 15) / 16) * 16;
   static constexpr size_t CL_BAR_OFF = CL_CTW_OFF + sizeof(float2) * CTW;
   static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 16 + 8;
   static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (TAILM ? HIST_BINS + CAND_SMEM + 4 : 0));
-  static constexpr int CL_MINB = T <= 256 ? 2 : 1;
+  static constexpr int CL_MINB = T <= 128 ? 3 : T <= 256 ? 2 : 1;
 };
 
 struct TailCtx {
@@ -464,7 +477,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   const int n_rg = a.n_rg;
   const int npan = n_rg / W;
 
-  copy_table_async(tw, a.tw, Cf::TW, t, T);     // waited for in the first FFT pass
+  copy_table_async(tw, a.tw, Cf::TWK + (Cf::TWK & 1), t, T);   // waited for in the first FFT pass
   for (int i = t; i < Cf::CTW; i += T) {         // exact (sincospif) cluster twiddle tables
     const uint32_t m = i < (1 << Cf::LO) ? (uint32_t)i : (uint32_t)(i - (1 << Cf::LO)) << Cf::LO;
     ctw[i] = expi_frac<-1>(m, (uint32_t)N);

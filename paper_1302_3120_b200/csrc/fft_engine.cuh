@@ -105,6 +105,14 @@ struct Engine {
     return o;
   }
   static constexpr int TW_TOTAL = tw_total();
+  // forward-order tables come first: kernels that only run forward-order passes (run_keep,
+  // run, run_from_smem) need just the first TW_FWD entries
+  static CSSAR_DEV constexpr int tw_fwd() {
+    int o = 0;
+    for (int q = 1; q < P; ++q) o += tw_size_of(lns<false>(q), lr<false>(q));
+    return o;
+  }
+  static constexpr int TW_FWD = tw_fwd();
 
   // fill the twiddle tables (one entry per thread-iteration; exact sincospif arguments)
   static CSSAR_DEV void build_tw(float2* tw, int t, int nthreads) {
