@@ -610,8 +610,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           z[p + 1][c] = make_float2(q.z, q.w);
         }
         cluster_twiddles2<C, Ops::DIR, LOGN, Cf::LO>(z[p], z[p + 1], (uint32_t)slot_k(p), ctw);
-        dft<C, Ops::DIR>(z[p]);
-        dft<C, Ops::DIR>(z[p + 1]);
+        dft_sr<C, Ops::DIR>(z[p]);
+        dft_sr<C, Ops::DIR>(z[p + 1]);
       }
     } else {
 #pragma unroll
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       for (int p = 0; p < PT; ++p) {
         const int k = slot_k(p);
         cluster_twiddles<C, Ops::DIR, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);   // w_N^{c k}
-        dft<C, Ops::DIR>(z[p]);                                          // z[q] = X[k + M q]
+        dft_sr<C, Ops::DIR>(z[p]);                                       // z[q] = X[k + M q]
       }
     }
     consume(z, misc + 40);
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
         const int pr = p * T + t;
         const int k = rank * (M / C) + pr / W;
-        dft<C, -1>(z[p]);                                              // forward DIF first stage
+        dft_sr<C, -1>(z[p]);                                           // forward DIF first stage
         cluster_twiddles<C, -1, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);     // w_N^{-q k}
       }
       cl_wait();                                   // peers are done with their scatter buffers

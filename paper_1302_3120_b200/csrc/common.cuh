@@ -81,6 +81,49 @@ CSSAR_DEV void dft(float2 (&v)[R]) {
   }
 }
 
+// v * w_N^k with w_N = exp(DIR 2 pi i / N), N | 32 (compile-time k after unrolling)
+template <int N, int DIR>
+CSSAR_DEV float2 twN(float2 v, int k) { return tw32<DIR>(v, (k * (32 / N)) & 31); }
+
+// Split-radix DFT of length R (power of two, R <= 32), natural order in and out, unscaled:
+//   X[k] = sum_n v[n] exp(DIR 2 pi i n k / R).  DIT split: U = DFT_{R/2}(v[2n]),
+//   Z = DFT_{R/4}(v[4n+1]), Z' = DFT_{R/4}(v[4n+3]); for k < R/4, a = w^k Z[k],
+//   b = w^{3k} Z'[k]:  X[k] = U[k] + (a + b),  X[k+R/2] = U[k] - (a + b),
+//   X[k+R/4] = U[k+R/4] + DIR i (a - b),  X[k+3R/4] = U[k+R/4] - DIR i (a - b).
+// Fewer twiddle multiplies than the radix-2 stages of dft<> (same additions).
+template <int R, int DIR>
+CSSAR_DEV void dft_sr(float2 (&v)[R]) {
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = a + b;
+    v[1] = a - b;
+  } else {
+    float2 u[R / 2], z[R / 4], zp[R / 4];
+#pragma unroll
+    for (int n = 0; n < R / 2; ++n) u[n] = v[2 * n];
+#pragma unroll
+    for (int n = 0; n < R / 4; ++n) {
+      z[n] = v[4 * n + 1];
+      zp[n] = v[4 * n + 3];
+    }
+    dft_sr<R / 2, DIR>(u);
+    dft_sr<R / 4, DIR>(z);
+    dft_sr<R / 4, DIR>(zp);
+#pragma unroll
+    for (int k = 0; k < R / 4; ++k) {
+      const float2 a = twN<R, DIR>(z[k], k), b = twN<R, DIR>(zp[k], 3 * k);
+      const float2 s = a + b, d = a - b;
+      const float2 id = DIR > 0 ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);   // DIR i (a - b)
+      v[k] = u[k] + s;
+      v[k + R / 2] = u[k] - s;
+      v[k + R / 4] = u[k + R / 4] + id;
+      v[k + 3 * R / 4] = u[k + R / 4] - id;
+    }
+  }
+}
+
 // exp(DIR * 2 pi i * num / den) for integers 0 <= num < den, den a power of two <= 2^24:
 // the argument 2*num/den is exact in fp32 and sincospif is accurate to ~1 ulp.
 template <int DIR>

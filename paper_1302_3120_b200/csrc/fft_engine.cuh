@@ -193,7 +193,11 @@ struct Engine {
           }
         }
       }
+#if defined(CSSAR_DFT_RADIX2)
       dft<R, DIR>(x);
+#else
+      dft_sr<R, DIR>(x);
+#endif
 #pragma unroll
       for (int r = 0; r < R; ++r) v[m * R + r] = x[r];
     }
