@@ -38,7 +38,9 @@ CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
     f = sigma == 0.f ? 1.0f : f;
   }
   f = (u > s2bits) ? f : 0.0f;                             // strict survival on the |b|^2 pattern
-  return make_float2(b.x * f, b.y * f);
+  // explicitly rounded product: an FMA contraction with the consumer (e.g. the first FFT
+  // butterfly) would make E(b) inside a kernel round differently from the X it returns
+  return make_float2(__fmul_rn(b.x, f), __fmul_rn(b.y, f));
 }
 
 CSSAR_DEV uint32_t mask_bit(const uint32_t* mask, int words, int row, int col) {
