@@ -73,12 +73,14 @@ struct AzShape {
   // (TAIL) hist, candidates, counters], 1024-byte aligned stages
   static constexpr int BM = M < 256 ? M : 256;             // TMA box rows (box dims <= 256)
   static constexpr uint32_t STAGE_BYTES = (uint32_t)(sizeof(float2) * M * W);
-  static constexpr size_t CL_TW_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0));
+  // RESID: + a TMA-loaded buffer of Y at the output rows k + M q ([q][k][w])
+  static constexpr size_t CL_Y_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0));
+  static constexpr size_t CL_TW_OFF = CL_Y_OFF + (R ? sizeof(float2) * (size_t)M * W : 0);
   static constexpr int LO = (LOGN + 1) / 2;                      // cluster twiddle table split
   static constexpr int CTW = (1 << LO) + (1 << (LOGN - LO));      // lo[2^LO] | hi[N / 2^LO]
   static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TWK + 15) / 16) * 16;
   static constexpr size_t CL_BAR_OFF = CL_CTW_OFF + sizeof(float2) * CTW;
-  static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 16 + 8;
+  static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 24 + 8;
   static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (TAILM ? HIST_BINS + CAND_SMEM + 4 : 0));
   static constexpr int CL_MINB = T <= 128 ? 3 : T <= 256 ? 2 : 1;
 };
@@ -433,7 +435,8 @@ using AzClShape = AzShape<LOGN, MODE == AZ_RESID, 0, MODE == AZ_TAIL>;
 
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
-    az_cluster_kernel(const AzArgs a, const __grid_constant__ CUtensorMap tm) {
+    az_cluster_kernel(const AzArgs a, const __grid_constant__ CUtensorMap tm,
+                      const __grid_constant__ CUtensorMap tmy) {
   using Cf = AzClShape<LOGN, MODE>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E, NS = Cf::NS, BM = Cf::BM;
   constexpr int N = M * C;
@@ -459,6 +462,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cf::CL_BAR_OFF);
   uint64_t* rfull = full + NS;                                     // pushes landed in rbuf
   uint64_t* xfull = full + NS + 1;                                 // RESID scatter landed in xbuf
+  uint64_t* yfull = full + NS + 2;                                 // RESID Y buffer landed
+  float2* ybuf = reinterpret_cast<float2*>(base + Cf::CL_Y_OFF);
   uint32_t* misc = reinterpret_cast<uint32_t*>(base + Cf::CL_MISC_OFF);   // [0..31] reduce, [32] base
   const int t = threadIdx.x;
   const int rank = (int)cluster_rank();
@@ -522,6 +527,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1u);
     mbar_init(rfull, 1u);
     mbar_init(xfull, 1u);
+    mbar_init(yfull, 1u);
     mbar_expect_tx(rfull, Cf::STAGE_BYTES);        // armed for the first panel
     if (RES) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -551,6 +557,27 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
             const int row = k + M * q;
             Ops::fetch2(a, row, col0 + w, (size_t)row * n_rg + col0 + w, ax[p][q], ax[p + 1][q]);
           }
+        }
+      } else if constexpr (RES) {
+        if (t == 0) {                              // Y of the output rows: C boxes {W, M/C} by TMA
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_expect_tx(yfull, Cf::STAGE_BYTES);
+          constexpr int BY = (M / C) < 256 ? (M / C) : 256;   // TMA box rows (<= 256)
+#pragma unroll 1
+          for (int q = 0; q < C; ++q)
+#pragma unroll 1
+            for (int by = 0; by < (M / C) / BY; ++by)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, 0, %3}], [%4];\n"
+                  ::"r"(smem_u32(ybuf + (q * (M / C) + by * BY) * W)), "l"(reinterpret_cast<uint64_t>(&tmy)),
+                  "r"(col0), "r"(rank * (M / C) + M * q + by * BY), "r"(smem_u32(yfull))
+                  : "memory");
+        }
+#pragma unroll
+        for (int p = 0; p < PT; ++p) {
+          const int w = slot_w(p), k = slot_k(p);
+#pragma unroll
+          for (int q = 0; q < C; ++q) ax[p][q].m = mask_bit(a.mask, a.mask_words, k + M * q, col0 + w);
         }
       } else {
 #pragma unroll
@@ -631,9 +658,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     cl_arrive();                                   // rbuf (and, RESID, last panel's xbuf) consumed
     if constexpr (RES) {
 #pragma unroll
+      mbar_wait_cta(yfull, (uint32_t)(it & 1));
       for (int p = 0; p < PT; ++p) {
 #pragma unroll
-        for (int q = 0; q < C; ++q) z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
+        for (int q = 0; q < C; ++q) {
+          ax[p][q].v = ybuf[q * (M / C) * W + p * T + t];
+          z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
+        }
         const int pr = p * T + t;
         const int k = rank * (M / C) + pr / W;
         dft_sr<C, -1>(z[p]);                                           // forward DIF first stage
@@ -758,6 +789,11 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   CUtensorMap tm;
   cudaError_t e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM);
   if (e != cudaSuccess) return e;
+  CUtensorMap tmy = tm;
+  if constexpr (MODE == AZ_RESID) {           // Y with consecutive rows ({col, 0, row}), box {W, 1, M/C}
+    e = make_az_tensor_map(&tmy, a.Y, n_rg, 1 << LOGN, 1, Cf::W, Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256);
+    if (e != cudaSuccess) return e;
+  }
   const int npan = n_rg / Cf::W;
   const int ncl = npan < max_cl ? npan : max_cl;
   cudaLaunchConfig_t cfg = {};
@@ -772,7 +808,7 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k, a, tm);
+  e = cudaLaunchKernelEx(&cfg, k, a, tm, tmy);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
