@@ -441,7 +441,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E, NS = Cf::NS, BM = Cf::BM;
   constexpr int N = M * C;
   constexpr bool RES = MODE == AZ_RESID;
-  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_TAIL || MODE == AZ_INV_MASK;
+  // BS (TAIL, one stage): b_{i-1} of the output rows arrives by TMA into the stage buffer once the
+  // local transform has read it; the next panel's stage load is issued after the epilogue
+  constexpr bool BS = MODE == AZ_TAIL && NS == 1;
+  constexpr bool AUX = MODE == AZ_RESID || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK;
   static_assert(C > 1, "cluster kernel");
   using En = typename Cf::En;
   using Ops = AzOps<MODE>;
@@ -602,7 +605,23 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     float2 v[E];
     En::template run_keep<Ops::DIR>(s, v, ld, tw);
     float2* const xbuf = Cf::XS ? s : xbuf0;
-    if constexpr (!Cf::XS) {
+    if constexpr (BS) {
+      __syncthreads();                             // stage read: bring in b_{i-1} of the output rows
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(yfull, Cf::STAGE_BYTES);
+        constexpr int BY = (M / C) < 256 ? (M / C) : 256;
+#pragma unroll 1
+        for (int q = 0; q < C; ++q)
+#pragma unroll 1
+          for (int by = 0; by < (M / C) / BY; ++by)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, 0, %3}], [%4];\n"
+                ::"r"(smem_u32(s + (q * (M / C) + by * BY) * W)), "l"(reinterpret_cast<uint64_t>(&tmy)),
+                "r"(col0), "r"(rank * (M / C) + M * q + by * BY), "r"(smem_u32(yfull))
+                : "memory");
+      }
+    } else if constexpr (!Cf::XS) {
       __syncthreads();                             // stage fully read: refill it NS panels ahead
       if (t == 0 && next < npan) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -698,22 +717,30 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     } else if constexpr (VEC) {
+      if constexpr (BS) mbar_wait_cta(yfull, (uint32_t)(it & 1));
 #pragma unroll
       for (int p = 0; p < PT; p += 2) {
         const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
+          if constexpr (BS) {
+            const float4 bq = *reinterpret_cast<const float4*>(s + (q * (M / C) + k - rank * (M / C)) * W + w);
+            ax[p][q].v = make_float2(bq.x, bq.y);
+            ax[p + 1][q].v = make_float2(bq.z, bq.w);
+          }
           Ops::epi2(a, (size_t)row * n_rg + col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc);
         }
       }
     } else {
+      if constexpr (BS) mbar_wait_cta(yfull, (uint32_t)(it & 1));
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
         const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
+          if constexpr (BS) ax[p][q].v = s[(q * (M / C) + k - rank * (M / C)) * W + w];
           Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
         }
       }
@@ -731,6 +758,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
         __syncthreads();
         if (t == 0) tc.scount[0] = 0u;
+      }
+    }
+    if constexpr (BS) {
+      __syncthreads();                             // every b of the panel read from the stage
+      if (t == 0 && next < npan) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(next, sidx);
       }
     }
   }
@@ -790,8 +824,10 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   cudaError_t e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM);
   if (e != cudaSuccess) return e;
   CUtensorMap tmy = tm;
-  if constexpr (MODE == AZ_RESID) {           // Y with consecutive rows ({col, 0, row}), box {W, 1, M/C}
-    e = make_az_tensor_map(&tmy, a.Y, n_rg, 1 << LOGN, 1, Cf::W, Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256);
+  if constexpr (MODE == AZ_RESID || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b (TAIL) with
+    // consecutive rows ({col, 0, row}), box {W, 1, min(M/C, 256)}
+    e = make_az_tensor_map(&tmy, MODE == AZ_RESID ? (const void*)a.Y : (const void*)a.b, n_rg, 1 << LOGN, 1, Cf::W,
+                           Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256);
     if (e != cudaSuccess) return e;
   }
   const int npan = n_rg / Cf::W;
