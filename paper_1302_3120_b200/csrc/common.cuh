@@ -199,6 +199,16 @@ CSSAR_DEV uint64_t quad_eval(const Quad& q, int32_t u) {
 // (sin.approx / cos.approx: absolute error ~5e-7; 5 issue slots).  CSSAR_PHASE_TABLE: the
 // earlier exact path, top 24 bits rounded -> 256-entry SMEM table x 2-term polynomial
 // (error < 2e-8, ~13 issue slots + a table load).
+// exp(+-2 pi i h / 2^32) for the top 32 bits h of a fixed-point phase (SFU path)
+template <bool CONJ>
+CSSAR_DEV float2 phase_from_hi32(uint32_t h) {
+  const float ang = (float)(int32_t)h * 1.4629180792671596e-09f;   // 2 pi / 2^32
+  float sn, cs;
+  asm("sin.approx.f32 %0, %1;" : "=f"(sn) : "f"(ang));
+  asm("cos.approx.f32 %0, %1;" : "=f"(cs) : "f"(ang));
+  return make_float2(cs, CONJ ? -sn : sn);
+}
+
 template <bool CONJ>
 CSSAR_DEV float2 phase_from_fixed(const float2* tab256, uint64_t P) {
 #if defined(CSSAR_PHASE_TABLE)

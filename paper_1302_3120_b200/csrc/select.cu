@@ -119,7 +119,11 @@ __global__ void __launch_bounds__(1024) sel_coarse_kernel(long long k, SelState*
         cnt[HIST_BINS - 1] > 0)
       st->nonfinite = 1u;
     if (hist[HIST_BINS + 1]) st->nonfinite = 1u;          // any rank saw NaN/Inf (multi-GPU sum)
+#if defined(CSSAR_FORCE_FALLBACK)
+    const bool ok = false;
+#else
     const bool ok = sb >= 0 && sb >= st->cand_lo && sb <= st->cand_hi && hist[HIST_BINS] == 0u;
+#endif
     if (ok) {
       st->need_full = 0;
       st->target_bin = sb;
