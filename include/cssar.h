@@ -117,7 +117,11 @@ int cssar_nccl_unique_id(void* id_out);
  * candidate buffer (~32.6 B per local sample). */
 int cssar_workspace_size(cssar_plan plan, size_t* bytes);
 /* Bind caller-owned workspace (device, 256-byte aligned).  Kept until rebound or the
- * plan is destroyed; the caller keeps it alive. */
+ * plan is destroyed; the caller keeps it alive.  world > 1: a collective call (every rank
+ * binds): the ranks map each other's transpose buffers through CUDA IPC (peer memory over
+ * NVLink) so the sweeps store their output straight into the destination ranks' slabs
+ * (fused transposes); if any rank cannot map its peers, all ranks keep NCCL all-to-all
+ * transposes (also forced by the environment variable CSSAR_MULTI_A2A). */
 int cssar_bind_workspace(cssar_plan plan, void* ws, size_t bytes);
 
 /* Y_out = Theta o G(X)   (A X, eq. 24).  X and Y_out may alias. */
@@ -134,8 +138,9 @@ int cssar_image(cssar_plan plan, const void* Y, const uint32_t* mask_bits, void*
  * CSSAR_ERR_NONFINITE if NaN/Inf were seen.  The iteration body is replayed as a CUDA
  * graph captured once per (pointers, params) and cached in the plan.
  * world > 1: Y, mask_bits, X_inout are this rank's row slabs; collective over the ranks
- * (all must call with the same prm).  Per iteration: 4 NCCL all-to-all transposes between
- * row slabs (range sweeps) and column slabs (azimuth sweeps), all-reduces of the
+ * (all must call with the same prm).  Per iteration: 4 transposes between row slabs (range
+ * sweeps) and column slabs (azimuth sweeps) — fused into the sweeps' epilogues as peer
+ * stores plus a one-word all-reduce barrier, or NCCL all-to-alls — and all-reduces of the
  * residual norm and of the select histograms; the log is global.  PROFILE_STAGES is
  * ignored.  Results are bitwise identical to world 1 (same kernels, same global indices;
  * only the floating-point order of the logged residual norm differs). */

@@ -1,5 +1,7 @@
 // libcssar C ABI (include/cssar.h): plan (S0 phase-coefficient table), operator calls and
 // the graph-replayed ITA loop.  Host code only; device work lives in kernels.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -76,6 +78,13 @@ struct cssar_plan_s {
   float2* bcol = nullptr;
   uint32_t* mcol = nullptr;         // mask bits of the column slab, ncol/32 words per line
   bool have_mask = false;
+  // fused transposes: every rank's Ucol / Vrow mapped in this process (peer memory over
+  // NVLink via CUDA IPC on a multi-GPU box; the other emulated ranks' buffers in a group)
+  bool fused = false;
+  float2* peerU[16] = {};
+  float2* peerV[16] = {};
+  void* ipc_base[16] = {};          // IPC mappings opened by this rank (closed on rebind/destroy)
+  uint32_t* d_bar = nullptr;        // 1-word all-reduce used as the inter-sweep barrier (NCCL)
 };
 
 namespace {
@@ -174,6 +183,7 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi load_nccl() {
@@ -193,9 +203,10 @@ NcclApi load_nccl() {
   NCCL_SYM(send, "ncclSend");
   NCCL_SYM(recv, "ncclRecv");
   NCCL_SYM(allReduce, "ncclAllReduce");
+  NCCL_SYM(allGather, "ncclAllGather");
 #undef NCCL_SYM
   a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv &&
-         a.allReduce;
+         a.allReduce && a.allGather;
   return a;
 }
 
@@ -396,6 +407,7 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s)
   void *U[16], *V[16], *B[16];
   gather_ptrs(R, U, [](cssar_plan q) { return q->Ucol; });
   gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
+  const bool fused = p0->fused;
   auto az = [&](int mode) -> int {
     for (int i = 0; i < R.np; ++i) {
       cssar_plan pl = R.pl[i];
@@ -403,6 +415,11 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s)
       a.in = mode == AZ_FWD_THR ? pl->bcol : pl->Ucol;
       a.out = pl->Ucol;
       if (mode == AZ_RESID) a.tw = pl->d_az_tab_r;
+      if (fused && mode != AZ_TAIL) {        // epilogue stores into every rank's row slab block
+        for (int q = 0; q < pl->world; ++q) a.dst[q] = pl->peerV[q];
+        a.dlog_nrow = ilog2_exact(pl->nrow);
+        a.drank = pl->rank;
+      }
       CUDA_TRY(launch_az(pl->log_naz, mode, a.n_rg, a, s));
     }
     return CSSAR_OK;
@@ -410,8 +427,21 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s)
   auto rg = [&](bool gbody) -> int {
     for (int i = 0; i < R.np; ++i) {
       cssar_plan pl = R.pl[i];
-      CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody, (int)pl->nrow, rg_row_args(pl), s));
+      RgArgs r = rg_row_args(pl);
+      if (fused) {                           // epilogue stores into every rank's column slab
+        for (int q = 0; q < pl->world; ++q) r.dst[q] = pl->peerU[q];
+        r.dlog_nrow = ilog2_exact(pl->nrow);
+        r.drank = pl->rank;
+      }
+      CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody, (int)pl->nrow, r, s));
     }
+    return CSSAR_OK;
+  };
+  // after a fused sweep: every rank's peer stores into us are complete (NCCL: a one-word
+  // all-reduce orders the ranks' streams; the emulation group is serialised on one stream)
+  auto barrier = [&]() -> int {
+    if (R.group()) return CSSAR_OK;
+    NCCL_TRY(nccl().allReduce(p0->d_bar, p0->d_bar, 1, ncclUint32, ncclSum, p0->comm, s));
     return CSSAR_OK;
   };
   auto local_sel = [&](int part) -> int {
@@ -424,14 +454,25 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s)
     return CSSAR_OK;
   };
 #define STEP(x) do { int _rc = (x); if (_rc != CSSAR_OK) return _rc; } while (0)
-  STEP(az(AZ_FWD_THR));                       // S1 on column slabs
-  STEP(xchg_a2a(R, U, V, blk, s));            //    -> blocked row slabs
-  STEP(rg(true));                             // S2
-  STEP(xchg_a2a(R, V, U, blk, s));            //    -> column slabs
-  STEP(az(AZ_RESID));                         // S3
-  STEP(xchg_a2a(R, U, V, blk, s));
-  STEP(rg(false));                            // S4
-  STEP(xchg_a2a(R, V, U, blk, s));
+  if (fused) {                                // compute + transpose in one kernel per sweep
+    STEP(az(AZ_FWD_THR));                     // S1: column slabs -> every rank's row slab
+    STEP(barrier());
+    STEP(rg(true));                           // S2: row slab -> every rank's column slab
+    STEP(barrier());
+    STEP(az(AZ_RESID));                       // S3
+    STEP(barrier());
+    STEP(rg(false));                          // S4
+    STEP(barrier());
+  } else {
+    STEP(az(AZ_FWD_THR));                     // S1 on column slabs
+    STEP(xchg_a2a(R, U, V, blk, s));          //    -> blocked row slabs
+    STEP(rg(true));                           // S2
+    STEP(xchg_a2a(R, V, U, blk, s));          //    -> column slabs
+    STEP(az(AZ_RESID));                       // S3
+    STEP(xchg_a2a(R, U, V, blk, s));
+    STEP(rg(false));                          // S4
+    STEP(xchg_a2a(R, V, U, blk, s));
+  }
   STEP(az(AZ_TAIL));                          // S5: local histogram / candidates / support
   gather_ptrs(R, B, [](cssar_plan q) { return reinterpret_cast<char*>(q->d_st) + offsetof(SelState, resid2); });
   STEP(xchg_allreduce(R, B, 2, 1, s));
@@ -617,6 +658,83 @@ const char* cssar_error_string(int code) {
 
 namespace {
 
+// ---- fused transposes on a multi-GPU box: map every rank's workspace through CUDA IPC
+void close_peers(cssar_plan pl) {
+  for (int q = 0; q < 16; ++q) {
+    if (pl->ipc_base[q]) cudaIpcCloseMemHandle(pl->ipc_base[q]);
+    pl->ipc_base[q] = nullptr;
+    pl->peerU[q] = pl->peerV[q] = nullptr;
+  }
+  pl->fused = false;
+}
+
+// collective over the plan's communicator; on any failure the plan keeps the NCCL
+// all-to-all transposes (fused = false) and says so on stderr
+int map_peers_nccl(cssar_plan pl) {
+  close_peers(pl);
+  if (std::getenv("CSSAR_MULTI_A2A")) return CSSAR_OK;
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&range), cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      range = nullptr;
+  }
+  struct Rec { cudaIpcMemHandle_t h; unsigned long long off; unsigned long long pad; };
+  static_assert(sizeof(Rec) % 16 == 0, "record size");
+  Rec mine{};
+  bool ok = range != nullptr;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (ok) ok = range(&base, &size, (CUdeviceptr)pl->ws) == CUDA_SUCCESS;
+  if (ok) ok = cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
+  mine.off = ok ? (unsigned long long)((CUdeviceptr)pl->ws - base) : ~0ull;
+  // every rank takes part in the all-gather even if its own mapping failed
+  Rec* d = nullptr;
+  std::vector<Rec> all((size_t)pl->world);
+  CUDA_TRY(cudaMalloc(&d, sizeof(Rec) * (size_t)(pl->world + 1)));
+  int rc = CSSAR_OK;
+  if (cudaMemcpy(d + pl->world, &mine, sizeof(Rec), cudaMemcpyHostToDevice) != cudaSuccess ||
+      nccl().allGather(d + pl->world, d, sizeof(Rec), ncclUint8, pl->comm, pl->cap_stream) != ncclSuccess ||
+      cudaStreamSynchronize(pl->cap_stream) != cudaSuccess ||
+      cudaMemcpy(all.data(), d, sizeof(Rec) * (size_t)pl->world, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = CSSAR_ERR_NCCL;
+  cudaFree(d);
+  if (rc != CSSAR_OK) return rc;
+  bool every = true;
+  for (const Rec& r : all) every = every && r.off != ~0ull;
+  const size_t voff = (size_t)((char*)pl->Vrow - (char*)pl->Ucol);
+  for (int q = 0; q < pl->world && every; ++q) {
+    if (q == pl->rank) {
+      pl->peerU[q] = pl->Ucol;
+      pl->peerV[q] = pl->Vrow;
+      continue;
+    }
+    void* pb = nullptr;
+    if (cudaIpcOpenMemHandle(&pb, all[(size_t)q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      every = false;
+      break;
+    }
+    pl->ipc_base[q] = pb;
+    pl->peerU[q] = reinterpret_cast<float2*>(static_cast<char*>(pb) + all[(size_t)q].off);
+    pl->peerV[q] = reinterpret_cast<float2*>(reinterpret_cast<char*>(pl->peerU[q]) + voff);
+  }
+  // all ranks must agree on the mode: all-reduce the failure flag
+  uint32_t bad = every ? 0u : 1u;
+  if (cudaMemcpy(pl->d_bar, &bad, 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+      nccl().allReduce(pl->d_bar, pl->d_bar, 1, ncclUint32, ncclSum, pl->comm, pl->cap_stream) != ncclSuccess ||
+      cudaStreamSynchronize(pl->cap_stream) != cudaSuccess ||
+      cudaMemcpy(&bad, pl->d_bar, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return CSSAR_ERR_NCCL;
+  if (bad) {
+    close_peers(pl);
+    std::fprintf(stderr, "libcssar: peer mapping unavailable; using NCCL all-to-all transposes\n");
+    return CSSAR_OK;
+  }
+  pl->fused = true;
+  return CSSAR_OK;
+}
+
 int validate_world(const cssar_sar_params& p, int world, int rank) {
   if (world < 1 || world > 16 || rank < 0 || rank >= world) return CSSAR_ERR_BAD_PLAN;
   if (world == 1) return CSSAR_OK;
@@ -670,6 +788,10 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
   }
   for (int i = 0; i < 7; ++i) {
     if (cudaEventCreate(&pl->ev[i]) == cudaSuccess) continue;
+    cssar_plan_destroy(pl);
+    return CSSAR_ERR_CUDA;
+  }
+  if (world > 1 && (cudaMalloc(&pl->d_bar, 16) != cudaSuccess || cudaMemset(pl->d_bar, 0, 16) != cudaSuccess)) {
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
@@ -748,6 +870,8 @@ int cssar_nccl_unique_id(void* id_out) {
 
 int cssar_plan_destroy(cssar_plan pl) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
+  close_peers(pl);
+  cudaFree(pl->d_bar);
   if (pl->comm && nccl().ok) nccl().commDestroy(pl->comm);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
@@ -781,6 +905,7 @@ int cssar_bind_workspace(cssar_plan pl, void* ws, size_t bytes) {
   bind_views(pl, (char*)ws);
   if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
   pl->ghave = false;
+  if (pl->transport == kTransportNccl) return map_peers_nccl(pl);   // collective
   return CSSAR_OK;
 }
 
@@ -836,6 +961,16 @@ int cssar_group_ita_iterate(cssar_group g, const void* const* Y, const uint32_t*
   }
   const int v = validate_ita(g->pl[0], prm);
   if (v != CSSAR_OK) return v;
+  const bool fused = std::getenv("CSSAR_MULTI_A2A") == nullptr;
+  for (int r = 0; r < P; ++r) {
+    cssar_plan pl = g->pl[(size_t)r];
+    for (int q = 0; q < P; ++q) {
+      pl->peerU[q] = g->pl[(size_t)q]->Ucol;
+      pl->peerV[q] = g->pl[(size_t)q]->Vrow;
+    }
+    if (pl->fused != fused) { g->ghave = false; }
+    pl->fused = fused;
+  }
   Ranks R{g->pl.data(), P};
   return ita_multi(R, Y, mask_bits, *prm, X_inout, log_host, (cudaStream_t)stream, &g->gexec, &g->gkey,
                    &g->ghave);

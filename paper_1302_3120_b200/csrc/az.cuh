@@ -101,6 +101,12 @@ struct Aux {
   uint32_t m;      // mask bit
 };
 
+// destination of output line `row`, column `col` (plain array or a rank's blocked row slab)
+CSSAR_DEV float2* out_at(const AzArgs& a, int row, int col) {
+  const int m = (1 << a.dlog_nrow) - 1;
+  return a.dst[row >> a.dlog_nrow] + ((size_t)((a.drank << a.dlog_nrow) + (row & m))) * (size_t)a.n_rg + col;
+}
+
 template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR) ? -1 : +1;   // first transform direction
@@ -156,8 +162,9 @@ struct AzOps {
   }
 
   // two adjacent columns: per-element epilogue, one 16-byte store
-  CSSAR_DEV static void epi2(const AzArgs& a, size_t idx, float2 x0, float2 x1, const Aux& a0, const Aux& a1,
+  CSSAR_DEV static void epi2(const AzArgs& a, int row, int col, float2 x0, float2 x1, const Aux& a0, const Aux& a1,
                              TailCtx& tc) {
+    const size_t idx = (size_t)row * a.n_rg + col;
     const float sc = DIR < 0 ? a.oscale : a.scale;
     float2 v0 = x0 * sc, v1 = x1 * sc;
     if constexpr (MODE == AZ_INV_MASK) {
@@ -172,7 +179,7 @@ struct AzOps {
       tail_stats(a, v0, tc);
       tail_stats(a, v1, tc);
     } else {
-      *reinterpret_cast<float4*>(a.out + idx) = make_float4(v0.x, v0.y, v1.x, v1.y);
+      *reinterpret_cast<float4*>(out_at(a, row, col)) = make_float4(v0.x, v0.y, v1.x, v1.y);
     }
   }
 
@@ -198,7 +205,8 @@ struct AzOps {
     }
   }
 
-  CSSAR_DEV static void epi(const AzArgs& a, size_t idx, float2 x, const Aux& ax, TailCtx& tc) {
+  CSSAR_DEV static void epi(const AzArgs& a, int row, int col, float2 x, const Aux& ax, TailCtx& tc) {
+    const size_t idx = (size_t)row * a.n_rg + col;
     float2 v = x * (DIR < 0 ? a.oscale : a.scale);        // forward outputs feed a range sweep
     if constexpr (MODE == AZ_INV_MASK) {
       if (!ax.m) v = make_float2(0.f, 0.f);
@@ -209,7 +217,7 @@ struct AzOps {
       a.b[idx] = bn;
       tail_stats(a, bn, tc);
     } else {
-      a.out[idx] = v;
+      *out_at(a, row, col) = v;
     }
   }
 };
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 #pragma unroll
         for (int r = 0; r < R0; ++r) {
           const int row = j + r * (M / R0);
-          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.oscale;
+          *out_at(a, row, col0 + w) = x[r] * a.oscale;
         }
       };
       En::template conv<+1>(s, ld, mid, st, tw);
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = j + r * (M / RL);
-          Ops::epi(a, (size_t)row * n_rg + col0 + w, x[r], ax[r], tc);
+          Ops::epi(a, row, col0 + w, x[r], ax[r], tc);
         }
       };
       En::template run<Ops::DIR>(s, ld, st, tw);
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = rank + C * (j + r * (M / RL));
-          a.out[(size_t)row * n_rg + col0 + w] = x[r] * a.oscale;
+          *out_at(a, row, col0 + w) = x[r] * a.oscale;
         }
       };
       En::template run_from_smem<-1>(xbuf, st, tw);
@@ -729,7 +737,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
             ax[p][q].v = make_float2(bq.x, bq.y);
             ax[p + 1][q].v = make_float2(bq.z, bq.w);
           }
-          Ops::epi2(a, (size_t)row * n_rg + col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc);
+          Ops::epi2(a, row, col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc);
         }
       }
     } else {
@@ -741,7 +749,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
           if constexpr (BS) ax[p][q].v = s[(q * (M / C) + k - rank * (M / C)) * W + w];
-          Ops::epi(a, (size_t)row * n_rg + col0 + w, z[p][q], ax[p][q], tc);
+          Ops::epi(a, row, col0 + w, z[p][q], ax[p][q], tc);
         }
       }
     }
@@ -850,8 +858,14 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
 }
 
 template <int LOGN, int MODE>
-static cudaError_t az_launch(int n_rg, const AzArgs& a, cudaStream_t s) {
+static cudaError_t az_launch(int n_rg, const AzArgs& a_in, cudaStream_t s) {
   using Cf = AzShape<LOGN, MODE == AZ_RESID>;
+  AzArgs a = a_in;
+  if (!a.dst[0]) {                       // plain output array (single rank / in-place paths)
+    a.dst[0] = a.out;
+    a.dlog_nrow = LOGN;
+    a.drank = 0;
+  }
   if constexpr (Cf::C > 1) {
     return az_cluster_launch<LOGN, MODE>(n_rg, a, s);
   } else {

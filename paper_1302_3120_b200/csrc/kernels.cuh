@@ -68,6 +68,13 @@ struct AzArgs {
   float scale;              // 1/sqrt(n_az)
   float oscale;             // factor on outputs that feed a range sweep: scale/n_rg (range IFFT norm folded in)
   const float2* tw;         // precomputed inter-pass twiddle tables of the az engine (global)
+  // output destinations (multi-GPU fused transpose): output line `row` of the
+  // column slab is stored at dst[row >> dlog_nrow] + ((drank << dlog_nrow) + (row & (nrow-1))) *
+  // n_rg + col, i.e. straight into block `drank` of rank q's blocked row slab (peer memory).
+  // dst[0] == nullptr: plain `out` (launch_az fills dst[0] = out, dlog_nrow = log2 n_az).
+  float2* dst[16];
+  int dlog_nrow;
+  int drank;
 };
 
 struct RgArgs {
@@ -80,6 +87,12 @@ struct RgArgs {
   // received from the all-to-all; log_w = log2(n_rg), blk = 0 is the plain row-major layout
   int log_w;
   long long blk;
+  // blocked layout only: if dst[0] != nullptr the output goes to the column slabs of the
+  // ranks instead of in place: sample j of local row r -> dst[j >> log_w] +
+  // ((drank << dlog_nrow) + r) * 2^log_w + (j & (2^log_w - 1))   (peer memory, fused transpose)
+  float2* dst[16];
+  int dlog_nrow;
+  int drank;
 };
 
 enum AzMode : int {

@@ -70,6 +70,18 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
     phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
+    if constexpr (BLK) {
+      if (a.dst[0]) {                      // fused transpose: straight into the ranks' column slabs
+        const int wm = (1 << a.log_w) - 1;
+        const size_t rowoff = (size_t)((a.drank << a.dlog_nrow) + row0 + b) << a.log_w;
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+          const int jj = j + r * (N / R0);
+          a.dst[jj >> a.log_w][rowoff + (size_t)(jj & wm)] = x[r];
+        }
+        return;
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });

@@ -1,13 +1,14 @@
 """The multi-GPU slab-partitioned ITA (include/cssar.h world > 1) on one device.
 
-cssar_group runs, for `world` emulated ranks, exactly the kernels and schedule of the NCCL
-path: row slabs of n_az/world azimuth lines for the range sweeps, column slabs of
-n_rg/world gates for the azimuth sweeps, four all-to-all transposes per iteration (device
-copies here, NCCL send/recv on a multi-GPU box) and the select's histograms summed over
-ranks.  Every kernel computes with global indices, so the result must be BITWISE equal to
-the single-GPU plan on the same inputs (only the summation order of the logged residual
-norm differs), and the single-GPU plan is itself pinned to the fp64 oracle
-(test_gpu_ita.py); one case also checks the oracle directly.
+cssar_group runs, for `world` emulated ranks, exactly the kernels and schedule of the
+multi-GPU path: row slabs of n_az/world azimuth lines for the range sweeps, column slabs of
+n_rg/world gates for the azimuth sweeps, the transposes fused into the sweeps' epilogues
+(stores into every rank's slab: the other emulated ranks' buffers here, CUDA-IPC peer memory
+over NVLink on a multi-GPU box; CSSAR_MULTI_A2A selects separate all-to-all transposes) and
+the select's histograms summed over ranks.  Every kernel computes with global indices, so
+the result must be BITWISE equal to the single-GPU plan on the same inputs (only the
+summation order of the logged residual norm differs), and the single-GPU plan is itself
+pinned to the fp64 oracle (test_gpu_ita.py); one case also checks the oracle directly.
 """
 import numpy as np
 import pytest
@@ -71,6 +72,20 @@ def test_group_is_bitwise_single_gpu(name, grid, world, iters):
     prob = problem(name, *(grid or (None, None)))
     Xs, ls = _single_run(prob, iters)
     Xg, lg = _group_run(prob, world, iters)
+    assert np.array_equal(Xg.view(np.uint32), Xs.view(np.uint32)), rel_l2(Xg, Xs)
+    _same_logs(lg, ls)
+
+
+@pytest.mark.parametrize("transport", ["fused", "a2a"])
+def test_group_transports_bitwise(transport, monkeypatch):
+    """Both exchange schedules of the multi-GPU path: the fused transposes (azimuth / range
+    epilogues store straight into every rank's slab — peer memory on a multi-GPU box) and
+    the separate all-to-all transposes (CSSAR_MULTI_A2A, the NCCL fallback)."""
+    if transport == "a2a":
+        monkeypatch.setenv("CSSAR_MULTI_A2A", "1")
+    prob = problem("c2", 1024, 1024)
+    Xs, ls = _single_run(prob, 6)
+    Xg, lg = _group_run(prob, 4, 6)
     assert np.array_equal(Xg.view(np.uint32), Xs.view(np.uint32)), rel_l2(Xg, Xs)
     _same_logs(lg, ls)
 
