@@ -16,6 +16,12 @@ Passages followed:
       h(t) = (2/3) t [1 + cos(2 pi/3 - (2/3) arccos((lm/8)(t/3)^(-3/2)))] for t > (54^(1/3)/4) lm^(2/3)
     written in the k-rule-normalised form with sigma = (54^(1/3)/4) lm^(2/3).
   * iteration count = number of X updates; output X_I (R18).
+  * adaptive step (NEXT-1; eq. 27, the strategy of the cited Blumensath2010):
+    mu_i = ||dX_k||^2 / ||Theta G(dX_k)||^2 with dX_k = dX on the support of X_i (DESIGN.md
+    R20) — the printed ratio is the reciprocal of a valid step (R11), so the
+    normalised-IHT form of the cited source is used; mu_i = 1 when the support is empty or
+    the denominator vanishes (S:L353).  With the k-rule sigma_i = |b|_(k+1) of b = X + mu_i dX;
+    with a fixed lambda sigma_i = lambda mu_i (soft) / the half jump point of lambda mu_i.
 """
 import numpy as np
 
@@ -76,11 +82,24 @@ def sigma_fixed_lambda(lam, mu, thr):
     return lm if thr == "soft" else half_sigma_from_lm(lm)
 
 
+def adaptive_mu(op, dX, X, mask):
+    """eq. 27 step (module docstring): ||dX_k||^2 / ||Theta G(dX_k)||^2, dX_k = dX on supp(X)."""
+    supp = np.asarray(X) != 0
+    if not supp.any():
+        return 1.0
+    dXk = np.where(supp, dX, 0.0)
+    num = float(np.vdot(dXk, dXk).real)
+    g = np.asarray(mask, dtype=np.float64) * op.G(dXk)
+    den = float(np.vdot(g, g).real)
+    return num / den if den > 0.0 and num > 0.0 else 1.0
+
+
 def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10, X0=None, log=None):
     """Algorithm 1 with A = Theta o G. Returns X_I (complex128).
 
     op: oracle.csa.CSAOperator; Y: echo (zero-filled where mask == 0); mask: 0/1 array.
-    log (optional list) receives per-iteration dicts: sigma, lam, support, resid2, gap, obj.
+    mu: a positive step, or "adaptive" for the eq. 27 rule (adaptive_mu).
+    log (optional list) receives per-iteration dicts: sigma, lam, mu, support, resid2, gap.
     """
     Y = np.asarray(Y, dtype=np.complex128)
     m = np.asarray(mask, dtype=np.float64)
@@ -88,16 +107,19 @@ def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10
     for _ in range(iters):
         R = m * (Y - op.G(X))                      # Residue (Alg. 1 line 2)
         dX = op.M(R)                               # MF on residue (line 3); Theta already applied
-        b = X + mu * dX                            # b_mu(x_i)
+        mu_i = adaptive_mu(op, dX, X, m) if mu == "adaptive" else mu
+        b = X + mu_i * dX                          # b_mu(x_i)
         if rule == "k":
             sigma = sigma_k_rule(b, k)
         else:
-            sigma = sigma_fixed_lambda(lam, mu, thr)
+            sigma = sigma_fixed_lambda(lam, mu_i, thr)
         Xn = threshold(b, sigma, thr)              # Thresholding (line 4)
         if log is not None:
             a = np.sort(np.abs(b).reshape(-1))[::-1]
-            entry = dict(sigma=float(sigma), support=int(np.count_nonzero(Xn)), resid2=float(np.vdot(R, R).real))
-            entry["lam"] = float(sigma / mu) if thr == "soft" else float(HALF_LM_PER_SIGMA32 * sigma ** 1.5 / mu)
+            entry = dict(sigma=float(sigma), mu=float(mu_i), support=int(np.count_nonzero(Xn)),
+                         resid2=float(np.vdot(R, R).real))
+            entry["lam"] = (float(sigma / mu_i) if thr == "soft"
+                            else float(HALF_LM_PER_SIGMA32 * sigma ** 1.5 / mu_i))
             if rule == "k":
                 entry["gap"] = float((a[k - 1] - a[k]) / a[k]) if a[k] > 0 else float("inf")
             log.append(entry)

@@ -176,3 +176,59 @@ def test_ita_recovers_c0_support():
     assert supp == set(prob.scene.idx.tolist())
     assert min(e["gap"] for e in log) > 1.0
     assert log[-1]["resid2"] < log[0]["resid2"]
+
+
+# ---------------------------------------------------------------- adaptive step (NEXT-1, eq. 27)
+def _dense_A(op, mask):
+    """A = Theta o G as an explicit matrix over vec(X) (columns = G of the basis images)."""
+    n_az, n_rg = op.shape
+    n = n_az * n_rg
+    A = np.zeros((n, n), np.complex128)
+    for j in range(n):
+        e = np.zeros(n, np.complex128)
+        e[j] = 1.0
+        A[:, j] = (np.asarray(mask, dtype=float) * op.G(e.reshape(n_az, n_rg))).reshape(-1)
+    return A
+
+
+def test_adaptive_mu_matches_dense_matrix_ratio():
+    """mu = ||v||^2 / ||A v||^2 for v = dX on supp(X), A the explicit (brute-force) matrix."""
+    p = SarParams(n_az=8, n_rg=16)
+    op = csa.CSAOperator(p)
+    mask = (np.random.default_rng(3).random((8, 16)) < 0.5).astype(float)
+    A = _dense_A(op, mask)
+    X = np.zeros((8, 16), np.complex128)
+    X.reshape(-1)[[3, 17, 40, 41, 99]] = _rand(5, 4)
+    dX = _rand((8, 16), 5)
+    v = np.where(X != 0, dX, 0).reshape(-1)
+    ref = np.vdot(v, v).real / np.vdot(A @ v, A @ v).real
+    assert abs(ita.adaptive_mu(op, dX, X, mask) - ref) <= 1e-12 * ref
+
+
+def test_adaptive_mu_bounds_and_special_cases():
+    """G unitary => ||Theta G v|| <= ||v||: mu >= 1, with equality at Theta = 1; an empty
+    support (X = 0, the first iteration of Algorithm 1) gives mu = 1."""
+    p = SarParams(n_az=32, n_rg=32)
+    op = csa.CSAOperator(p)
+    X = np.zeros((32, 32), np.complex128)
+    X.reshape(-1)[np.random.default_rng(6).choice(1024, 60, replace=False)] = 1.0 + 0.5j
+    dX = _rand((32, 32), 7)
+    assert abs(ita.adaptive_mu(op, dX, X, np.ones((32, 32))) - 1.0) <= 1e-12
+    for rate in (0.3, 0.6, 0.9):
+        mask = (np.random.default_rng(int(rate * 10)).random((32, 32)) < rate).astype(float)
+        assert ita.adaptive_mu(op, dX, X, mask) >= 1.0 - 1e-12
+    assert ita.adaptive_mu(op, dX, np.zeros((32, 32)), mask) == 1.0
+
+
+def test_adaptive_ita_equals_fixed_step_at_full_sampling():
+    """Theta = 1: every mu_i is 1, so the adaptive run reproduces mu = 1 (closed form)."""
+    cfg = configs.get("c0")
+    prob = synth.make_problem(cfg, lambda s, c: echo.exact_echo(c.params, s.targets))
+    op = csa.CSAOperator(cfg.params)
+    full = np.ones(prob.mask.shape)
+    Y = prob.Y.astype(np.complex128)
+    log = []
+    Xa = ita.ita(op, Y, full, thr="soft", rule="k", k=cfg.k, mu="adaptive", iters=4, log=log)
+    Xf = ita.ita(op, Y, full, thr="soft", rule="k", k=cfg.k, mu=1.0, iters=4)
+    assert all(abs(e["mu"] - 1.0) <= 1e-12 for e in log)
+    assert np.max(np.abs(Xa - Xf)) <= 1e-12 * np.max(np.abs(Xf))
