@@ -64,10 +64,15 @@ typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 
 /* flags: CSSAR_FLAG_PROFILE_STAGES launches the iteration body directly (no graph) with CUDA
  * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
  * accumulates per-step device time (read with cssar_stage_times). */
-enum { CSSAR_FLAG_PROFILE_STAGES = 1 };
+enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2 };
 
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
- * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule. */
+ * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule.
+ * CSSAR_FLAG_ADAPTIVE_MU (world 1 only; NEXT-1): mu is ignored and every iteration uses
+ * mu_i = ||dX_k||^2 / ||Theta G(dX_k)||^2, dX_k = the MF update M(Theta(Y - G X_i)) on the
+ * support of X_i (eq. 27, in the normalised-IHT form of its cited source;
+ * DESIGN.md R11, R20), mu_i = 1 on an empty support; the fixed-lambda rule then thresholds at
+ * lambda mu_i.  Costs three more sweeps and an elementwise pass per iteration. */
 typedef struct {
   int32_t thr;      /* cssar_thr */
   int32_t rule;     /* cssar_rule */
@@ -79,12 +84,13 @@ typedef struct {
 } cssar_ita_params;
 
 /* Per-iteration log (SPEC "SolverReport"): sigma_i = lambda_i mu_i, lambda_i,
- * support = #{|b_i| > sigma_i} (= #nonzeros of X_(i+1)), resid2 = ||Theta(Y - G X_i)||^2. */
+ * support = #{|b_i| > sigma_i} (= #nonzeros of X_(i+1)), resid2 = ||Theta(Y - G X_i)||^2, mu_i. */
 typedef struct {
   float sigma;
   float lambda;
   int64_t support;
   double resid2;
+  float mu;         /* step of the iteration (the fixed mu, or mu_i of the adaptive rule) */
 } cssar_iter_log;
 
 typedef struct cssar_plan_s* cssar_plan;
@@ -111,8 +117,9 @@ int cssar_plan_destroy(cssar_plan plan);
 /* Fill id_out (host, 128 bytes) with a fresh ncclUniqueId for cssar_plan_create(world > 1). */
 int cssar_nccl_unique_id(void* id_out);
 
-/* Bytes of device workspace cssar_ita_iterate needs: world 1: one complex64 array of the
- * scene size plus a candidate buffer for the exact top-k select (~8.5 B/sample); world > 1:
+/* Bytes of device workspace cssar_ita_iterate needs: world 1: two complex64 arrays of the
+ * scene size (transform buffer; adaptive-step gradient) plus a candidate buffer for the exact
+ * top-k select (~16.5 B/sample); world > 1:
  * four complex64 column-slab arrays (transposes, Y, state), the column-slab mask and the
  * candidate buffer (~32.6 B per local sample). */
 int cssar_workspace_size(cssar_plan plan, size_t* bytes);

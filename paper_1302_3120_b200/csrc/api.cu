@@ -54,6 +54,7 @@ struct cssar_plan_s {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   float2* U = nullptr;
+  float2* D = nullptr;              // adaptive step: the dense gradient dX (world 1)
   uint32_t* cand = nullptr;
   uint32_t cand_cap = 0;
   // graph cache for the iteration body
@@ -301,9 +302,24 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   // S4: M body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
   MARK(4);
-  // S5: F_eta^-1 ; b_i = X_i + mu dX ; |b|^2 histogram + candidates
   a.b = b;
-  CUDA_TRY(launch_az(pl->log_naz, AZ_TAIL, a.n_rg, a, s));
+  if (prm.flags & CSSAR_FLAG_ADAPTIVE_MU) {
+    // S5 (adaptive step, eq. 27): dX = F_eta^-1 u kept in D, F_eta(dX on supp X_i), ||dX_k||^2;
+    // G body; ||Theta o F_eta^-1 .||^2; mu_i = ratio; b_i = X_i + mu_i dX (+ histogram)
+    a.in = pl->U;
+    a.out = pl->U;
+    a.D = pl->D;
+    a.lambda = (float)prm.lambda;
+    a.tw = pl->d_az_tab_r;
+    CUDA_TRY(launch_az(pl->log_naz, AZ_GRAD, a.n_rg, a, s));
+    a.tw = pl->d_az_tab;
+    CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
+    CUDA_TRY(launch_az(pl->log_naz, AZ_NORM, a.n_rg, a, s));
+    CUDA_TRY(launch_adaptive_step(a, pl->n, pl->sm_count, s));
+  } else {
+    // S5: F_eta^-1 ; b_i = X_i + mu dX ; |b|^2 histogram + candidates
+    CUDA_TRY(launch_az(pl->log_naz, AZ_TAIL, a.n_rg, a, s));
+  }
   MARK(5);
   // S6: sigma_i (k-rule select or fixed lambda)
   CUDA_TRY(launch_select(pl->sm_count, b, pl->n, prm.k, prm.rule, prm.thr, (float)prm.mu, pl->d_st, pl->d_hist,
@@ -580,6 +596,7 @@ int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
   if (prm->rule == CSSAR_RULE_FIXED_LAMBDA && (!(prm->lambda >= 0.0) || !std::isfinite(prm->lambda)))
     return CSSAR_ERR_BAD_MU;
   if (prm->iters < 0 || prm->iters > kLogCap) return CSSAR_ERR_INVALID_PARAMS;
+  if ((prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && pl->world != 1) return CSSAR_ERR_INVALID_PARAMS;
   return CSSAR_OK;
 }
 
@@ -627,6 +644,7 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
       log_host[i].lambda = tmp[i].lam;
       log_host[i].support = tmp[i].support;
       log_host[i].resid2 = tmp[i].resid2;
+      log_host[i].mu = tmp[i].mu;
     }
     if (st.nonfinite) return CSSAR_ERR_NONFINITE;
   }
@@ -814,7 +832,7 @@ size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
 
 // workspace layout: world 1: [U | cand]; world > 1: [Ucol | Vrow | Ycol | bcol | mcol | cand]
 size_t workspace_bytes(cssar_plan pl) {
-  if (pl->world == 1) return sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
+  if (pl->world == 1) return 2 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
   return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + sizeof(uint32_t) * cand_capacity((long long)nl) + 256;
 }
@@ -822,7 +840,8 @@ size_t workspace_bytes(cssar_plan pl) {
 void bind_views(cssar_plan pl, char* ws) {
   if (pl->world == 1) {
     pl->U = (float2*)ws;
-    pl->cand = (uint32_t*)(ws + sizeof(float2) * (size_t)pl->n);
+    pl->D = (float2*)(ws + sizeof(float2) * (size_t)pl->n);
+    pl->cand = (uint32_t*)(ws + 2 * sizeof(float2) * (size_t)pl->n);
     pl->cand_cap = (uint32_t)cand_capacity(pl->n);
     return;
   }
@@ -1054,6 +1073,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       log_host[i].lambda = tmp[i].lam;
       log_host[i].support = tmp[i].support;
       log_host[i].resid2 = tmp[i].resid2;
+      log_host[i].mu = tmp[i].mu;
     }
     if (st.nonfinite) return CSSAR_ERR_NONFINITE;
   }

@@ -110,6 +110,11 @@ CSSAR_DEV float2* out_at(const AzArgs& a, int row, int col) {
 template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR) ? -1 : +1;   // first transform direction
+  // kernels that reduce a squared norm into the solver state
+  static constexpr bool RED = MODE == AZ_RESID || MODE == AZ_GRAD || MODE == AZ_NORM;
+  CSSAR_DEV static double* red_target(const AzArgs& a) {
+    return MODE == AZ_RESID ? &a.st->resid2 : MODE == AZ_GRAD ? &a.st->mu_num : &a.st->mu_den;
+  }
 
   // prologue on a loaded input value (loads are issued for a whole group first)
   CSSAR_DEV static float2 pro(const AzArgs& a, int row, int col, float2 v, uint32_t s2, float sig) {
@@ -125,9 +130,9 @@ struct AzOps {
     if constexpr (MODE == AZ_RESID) {
       x.m = mask_bit(a.mask, a.mask_words, row, col);
       x.v = __ldg(a.Y + idx);
-    } else if constexpr (MODE == AZ_INV_MASK) {
+    } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
       x.m = mask_bit(a.mask, a.mask_words, row, col);
-    } else if constexpr (MODE == AZ_TAIL) {
+    } else if constexpr (MODE == AZ_TAIL || MODE == AZ_GRAD) {
       x.v = a.b[idx];
     }
     return x;
@@ -141,7 +146,7 @@ struct AzOps {
       const float4 q = *reinterpret_cast<const float4*>(a.b + idx);
       x0.v = make_float2(q.x, q.y);
       x1.v = make_float2(q.z, q.w);
-    } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_RESID) {
+    } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_RESID || MODE == AZ_NORM) {
       const uint32_t wd = a.mask ? __ldg(a.mask + (size_t)row * a.mask_words + (col >> 5)) : 0xFFFFFFFFu;
       x0.m = (wd >> (col & 31)) & 1u;
       x1.m = (wd >> ((col + 1) & 31)) & 1u;
@@ -153,25 +158,38 @@ struct AzOps {
     }
   }
 
-  // RESID mid: g = G(X) sample; r = Theta o (Y - g)
-  CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc) {
-    const float2 g = x * a.scale;
-    const float2 r = ax.m ? (ax.v - g) : make_float2(0.f, 0.f);
-    acc = fmaf(r.x, r.x, fmaf(r.y, r.y, acc));
-    return r;
+  // RESID mid: g = G(X) sample; r = Theta o (Y - g).  GRAD mid (ax.v = b_{i-1}): dX = the
+  // sample, kept in D; returns dX on supp(X_i) = {|b_{i-1}|^2 > sigma_{i-1}^2} (R20)
+  CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc, int row, int col, uint32_t s2) {
+    if constexpr (MODE == AZ_GRAD) {
+      const float2 d = x * a.scale;
+      a.D[(size_t)row * a.n_rg + col] = d;
+      const float2 z = mag2_bits(ax.v) > s2 ? d : make_float2(0.f, 0.f);
+      acc = fmaf(z.x, z.x, fmaf(z.y, z.y, acc));
+      return z;
+    } else {
+      (void)row; (void)col; (void)s2;
+      const float2 g = x * a.scale;
+      const float2 r = ax.m ? (ax.v - g) : make_float2(0.f, 0.f);
+      acc = fmaf(r.x, r.x, fmaf(r.y, r.y, acc));
+      return r;
+    }
   }
 
   // two adjacent columns: per-element epilogue, one 16-byte store
   CSSAR_DEV static void epi2(const AzArgs& a, int row, int col, float2 x0, float2 x1, const Aux& a0, const Aux& a1,
-                             TailCtx& tc) {
+                             TailCtx& tc, float& acc) {
     const size_t idx = (size_t)row * a.n_rg + col;
     const float sc = DIR < 0 ? a.oscale : a.scale;
     float2 v0 = x0 * sc, v1 = x1 * sc;
-    if constexpr (MODE == AZ_INV_MASK) {
+    if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
       if (!a0.m) v0 = make_float2(0.f, 0.f);
       if (!a1.m) v1 = make_float2(0.f, 0.f);
     }
-    if constexpr (MODE == AZ_TAIL) {
+    if constexpr (MODE == AZ_NORM) {
+      acc = fmaf(v0.x, v0.x, fmaf(v0.y, v0.y, acc));
+      acc = fmaf(v1.x, v1.x, fmaf(v1.y, v1.y, acc));
+    } else if constexpr (MODE == AZ_TAIL) {
       const float2 k0 = threshold(a0.v, tc.s2bits, tc.sigma, a.thr), k1 = threshold(a1.v, tc.s2bits, tc.sigma, a.thr);
       v0 = make_float2(fmaf(a.mu, v0.x, k0.x), fmaf(a.mu, v0.y, k0.y));
       v1 = make_float2(fmaf(a.mu, v1.x, k1.x), fmaf(a.mu, v1.y, k1.y));
@@ -205,13 +223,15 @@ struct AzOps {
     }
   }
 
-  CSSAR_DEV static void epi(const AzArgs& a, int row, int col, float2 x, const Aux& ax, TailCtx& tc) {
+  CSSAR_DEV static void epi(const AzArgs& a, int row, int col, float2 x, const Aux& ax, TailCtx& tc, float& acc) {
     const size_t idx = (size_t)row * a.n_rg + col;
     float2 v = x * (DIR < 0 ? a.oscale : a.scale);        // forward outputs feed a range sweep
-    if constexpr (MODE == AZ_INV_MASK) {
+    if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
       if (!ax.m) v = make_float2(0.f, 0.f);
     }
-    if constexpr (MODE == AZ_TAIL) {
+    if constexpr (MODE == AZ_NORM) {
+      acc = fmaf(v.x, v.x, fmaf(v.y, v.y, acc));
+    } else if constexpr (MODE == AZ_TAIL) {
       const float2 xk = threshold(ax.v, tc.s2bits, tc.sigma, a.thr);     // X_i recomputed
       const float2 bn = make_float2(fmaf(a.mu, v.x, xk.x), fmaf(a.mu, v.y, xk.y));
       a.b[idx] = bn;
@@ -223,10 +243,10 @@ struct AzOps {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
-                                  (MODE == AZ_RESID && AzShape<LOGN, true>::MINB > 2) ? 2 : AzShape<LOGN, MODE == AZ_RESID>::MINB)
+__global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>::T,
+                                  ((MODE == AZ_RESID || MODE == AZ_GRAD) && AzShape<LOGN, true>::MINB > 2) ? 2 : AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>::MINB)
     az_kernel(const AzArgs a) {
-  using Cf = AzShape<LOGN, MODE == AZ_RESID>;
+  using Cf = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
   using En = typename Cf::En;
@@ -263,7 +283,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 
   uint32_t s2 = 0u;
   float sig = 0.f;
-  if constexpr (MODE == AZ_FWD_THR) {
+  if constexpr (MODE == AZ_FWD_THR || MODE == AZ_GRAD) {
     s2 = a.st->sigma2_bits;
     sig = a.st->sigma;
   }
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 
   static_assert(C == 1, "cluster shapes use az_cluster_kernel");
   {
-    if constexpr (MODE == AZ_RESID) {
+    if constexpr (MODE == AZ_RESID || MODE == AZ_GRAD) {
       auto mid = [&](int w, int j, float2* x) {
         Aux ax[RL];
 #pragma unroll
@@ -290,7 +310,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
           ax[r] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
         }
 #pragma unroll
-        for (int r = 0; r < RL; ++r) x[r] = Ops::mid(a, x[r], ax[r], racc);
+        for (int r = 0; r < RL; ++r) x[r] = Ops::mid(a, x[r], ax[r], racc, j + r * (M / RL), col0 + w, s2);
       };
       auto st = [&](int w, int j, float2* x) {
 #pragma unroll
@@ -311,15 +331,15 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int row = j + r * (M / RL);
-          Ops::epi(a, row, col0 + w, x[r], ax[r], tc);
+          Ops::epi(a, row, col0 + w, x[r], ax[r], tc, racc);
         }
       };
       En::template run<Ops::DIR>(s, ld, st, tw);
     }
   }
 
-  if constexpr (MODE == AZ_RESID) {
-    // block reduce ||r||^2 -> one double atomic per CTA
+  if constexpr (Ops::RED) {
+    // block reduce the squared norm -> one double atomic per CTA
     __shared__ float red[32];
     float v = racc;
 #pragma unroll
@@ -330,7 +350,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID>::T,
       float u = (t < T / 32) ? red[t] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-      if (t == 0) atomicAdd(&a.st->resid2, (double)u);
+      if (t == 0) atomicAdd(Ops::red_target(a), (double)u);
     }
   }
   if constexpr (MODE == AZ_TAIL) {
@@ -439,7 +459,7 @@ CSSAR_DEV void mbar_wait_cta(const uint64_t* bar, uint32_t parity) {
 }
 
 template <int LOGN, int MODE>
-using AzClShape = AzShape<LOGN, MODE == AZ_RESID, 0, MODE == AZ_TAIL>;
+using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, MODE == AZ_TAIL>;
 
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
@@ -448,11 +468,12 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   using Cf = AzClShape<LOGN, MODE>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E, NS = Cf::NS, BM = Cf::BM;
   constexpr int N = M * C;
-  constexpr bool RES = MODE == AZ_RESID;
+  constexpr bool RES = MODE == AZ_RESID || MODE == AZ_GRAD;   // two transforms, scatter
   // BS (TAIL, one stage): b_{i-1} of the output rows arrives by TMA into the stage buffer once the
   // local transform has read it; the next panel's stage load is issued after the epilogue
   constexpr bool BS = MODE == AZ_TAIL && NS == 1;
-  constexpr bool AUX = MODE == AZ_RESID || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK;
+  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK ||
+                      MODE == AZ_NORM;
   static_assert(C > 1, "cluster kernel");
   using En = typename Cf::En;
   using Ops = AzOps<MODE>;
@@ -514,7 +535,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   }
   uint32_t s2 = 0u;
   float sig = 0.f;
-  if constexpr (MODE == AZ_FWD_THR) {
+  if constexpr (MODE == AZ_FWD_THR || MODE == AZ_GRAD) {
     s2 = a.st->sigma2_bits;
     sig = a.st->sigma;
   }
@@ -584,11 +605,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
                   "r"(col0), "r"(rank * (M / C) + M * q + by * BY), "r"(smem_u32(yfull))
                   : "memory");
         }
+        if constexpr (MODE == AZ_RESID) {
 #pragma unroll
-        for (int p = 0; p < PT; ++p) {
-          const int w = slot_w(p), k = slot_k(p);
+          for (int p = 0; p < PT; ++p) {
+            const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
-          for (int q = 0; q < C; ++q) ax[p][q].m = mask_bit(a.mask, a.mask_words, k + M * q, col0 + w);
+            for (int q = 0; q < C; ++q) ax[p][q].m = mask_bit(a.mask, a.mask_words, k + M * q, col0 + w);
+          }
         }
       } else {
 #pragma unroll
@@ -690,7 +713,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           ax[p][q].v = ybuf[q * (M / C) * W + p * T + t];
-          z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc);
+          z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc, slot_k(p) + M * q, col0 + slot_w(p), s2);
         }
         const int pr = p * T + t;
         const int k = rank * (M / C) + pr / W;
@@ -737,7 +760,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
             ax[p][q].v = make_float2(bq.x, bq.y);
             ax[p + 1][q].v = make_float2(bq.z, bq.w);
           }
-          Ops::epi2(a, row, col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc);
+          Ops::epi2(a, row, col0 + w, z[p][q], z[p + 1][q], ax[p][q], ax[p + 1][q], tc, racc);
         }
       }
     } else {
@@ -749,7 +772,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         for (int q = 0; q < C; ++q) {
           const int row = k + M * q;
           if constexpr (BS) ax[p][q].v = s[(q * (M / C) + k - rank * (M / C)) * W + w];
-          Ops::epi(a, row, col0 + w, z[p][q], ax[p][q], tc);
+          Ops::epi(a, row, col0 + w, z[p][q], ax[p][q], tc, racc);
         }
       }
     }
@@ -778,7 +801,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   }
 
   if (it > 0) cl_wait();                           // pairs with the last arrive
-  if constexpr (MODE == AZ_RESID) {
+  if constexpr (Ops::RED) {
     float v = racc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -789,7 +812,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       float u = (t < T / 32) ? reinterpret_cast<float*>(misc)[t] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-      if (t == 0) atomicAdd(&a.st->resid2, (double)u);
+      if (t == 0) atomicAdd(Ops::red_target(a), (double)u);
     }
   }
   if constexpr (MODE == AZ_TAIL) {
@@ -832,7 +855,7 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   cudaError_t e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM);
   if (e != cudaSuccess) return e;
   CUtensorMap tmy = tm;
-  if constexpr (MODE == AZ_RESID || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b (TAIL) with
+  if constexpr (MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b with
     // consecutive rows ({col, 0, row}), box {W, 1, min(M/C, 256)}
     e = make_az_tensor_map(&tmy, MODE == AZ_RESID ? (const void*)a.Y : (const void*)a.b, n_rg, 1 << LOGN, 1, Cf::W,
                            Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256);
@@ -859,7 +882,7 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
 
 template <int LOGN, int MODE>
 static cudaError_t az_launch(int n_rg, const AzArgs& a_in, cudaStream_t s) {
-  using Cf = AzShape<LOGN, MODE == AZ_RESID>;
+  using Cf = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>;
   AzArgs a = a_in;
   if (!a.dst[0]) {                       // plain output array (single rank / in-place paths)
     a.dst[0] = a.out;
@@ -920,6 +943,8 @@ cudaError_t az_dispatch_mode(int mode, int n_rg, const AzArgs& a, cudaStream_t s
     case AZ_INV_MASK: return az_launch<LOGN, AZ_INV_MASK>(n_rg, a, s);
     case AZ_RESID: return az_launch<LOGN, AZ_RESID>(n_rg, a, s);
     case AZ_TAIL: return az_launch<LOGN, AZ_TAIL>(n_rg, a, s);
+    case AZ_GRAD: return az_launch<LOGN, AZ_GRAD>(n_rg, a, s);
+    case AZ_NORM: return az_launch<LOGN, AZ_NORM>(n_rg, a, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -46,9 +46,14 @@ struct SelState {
   uint32_t fine_prefix;     // split fine select (multi-GPU): matched high bits so far
   uint32_t fine_rank;       //   rank inside the current prefix
   unsigned long long fine_abv;  //   elements strictly above the prefix
+  // adaptive step (NEXT-1, eq. 27): mu_i = mu_num / mu_den, 0 = fixed mu (prm.mu)
+  double mu_num;            // ||dX_k||^2 (AZ_GRAD)
+  double mu_den;            // ||Theta G(dX_k)||^2 (AZ_NORM)
+  float mu;                 // mu_i of the current iteration (adaptive runs), else 0
+  float lambda;             // fixed-lambda rule: lambda (adaptive runs recompute sigma = f(lambda mu_i))
 };
 
-struct IterLogDev { float sigma; float lam; long long support; double resid2; };
+struct IterLogDev { float sigma; float lam; long long support; double resid2; float mu; };
 
 struct AzArgs {
   const float2* in;
@@ -75,6 +80,8 @@ struct AzArgs {
   float2* dst[16];
   int dlog_nrow;
   int drank;
+  float2* D;                // AZ_GRAD: dense gradient dX (for the elementwise step)
+  float lambda;             // fixed-lambda rule with the adaptive step (sigma_i = f(lambda mu_i))
 };
 
 struct RgArgs {
@@ -103,6 +110,8 @@ enum AzMode : int {
   AZ_INV_MASK = 4,    // Theta o F_eta^-1 u
   AZ_RESID = 5,       // F_eta Theta o (Y - F_eta^-1 u)               (S3)
   AZ_TAIL = 6,        // b <- E(b; sigma) + mu F_eta^-1 u, histogram  (S5)
+  AZ_GRAD = 7,        // adaptive step: dX = F_eta^-1 u -> D; F_eta (dX on supp X_i); ||dX_k||^2
+  AZ_NORM = 8,        // adaptive step: ||Theta o F_eta^-1 u||^2 only
 };
 
 // host-side launchers (kernels.cu)
@@ -124,6 +133,9 @@ cudaError_t launch_select_part(int part, int sm_count, float2* b, long long n, l
                                SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand,
                                uint32_t cand_cap, uint32_t* lvl, IterLogDev* log, int log_cap, cudaStream_t s);
 cudaError_t launch_lambda_step(SelState* st, int thr, float mu, IterLogDev* log, int log_cap, cudaStream_t s);
+// adaptive step: mu_i = mu_num/mu_den (1 if either is 0); b <- E(b; sigma_{i-1}) + mu_i D; histogram /
+// candidates / fixed-lambda support exactly as the tail kernel
+cudaError_t launch_adaptive_step(const AzArgs& a, long long n, int sm_count, cudaStream_t s);
 // bufs[p][i] <- sum_p bufs[p][i] for every p (single-device emulation of an all-reduce)
 cudaError_t launch_group_sum(int dtype, void* const* bufs, int world, long long count, cudaStream_t s);
 cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,

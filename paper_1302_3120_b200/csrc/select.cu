@@ -219,7 +219,9 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
     if (it < log_cap) {
       IterLogDev e;
       e.sigma = sig;
-      e.lam = thr == THR_SOFT ? sig / mu : (float)(1.0886621079036347 * pow((double)sig, 1.5) / mu);
+      const float m = st->mu > 0.f ? st->mu : mu;          // adaptive step of this iteration
+      e.mu = m;
+      e.lam = thr == THR_SOFT ? sig / m : (float)(1.0886621079036347 * pow((double)sig, 1.5) / m);
       e.support = (long long)abv;
       e.resid2 = st->resid2;
       log[it] = e;
@@ -232,6 +234,8 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
     st->cand_count = 0u;
     st->cand_overflow = 0u;
     st->resid2 = 0.0;
+    st->mu_num = 0.0;
+    st->mu_den = 0.0;
   }
   const int nf = st->need_full;
   __syncthreads();
@@ -332,11 +336,13 @@ __global__ void __launch_bounds__(1024) fine_find_kernel(int lvl, int thr, float
 
 __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* log, int log_cap) {
   const int it = st->iter;
+  const float m = st->mu > 0.f ? st->mu : mu;      // adaptive runs: sigma_fixed already = f(lambda mu_i)
   if (it < log_cap) {
     IterLogDev e;
     e.sigma = st->sigma_fixed;
-    e.lam = thr == THR_SOFT ? st->sigma_fixed / mu
-                            : (float)(1.0886621079036347 * pow((double)st->sigma_fixed, 1.5) / mu);
+    e.mu = m;
+    e.lam = thr == THR_SOFT ? st->sigma_fixed / m
+                            : (float)(1.0886621079036347 * pow((double)st->sigma_fixed, 1.5) / m);
     e.support = (long long)st->support_fixed;
     e.resid2 = st->resid2;
     log[it] = e;
@@ -346,6 +352,8 @@ __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* 
   st->sigma = st->sigma_fixed;
   st->support_fixed = 0ull;
   st->resid2 = 0.0;
+  st->mu_num = 0.0;
+  st->mu_den = 0.0;
 }
 
 __global__ void init_state_kernel(SelState* st, uint32_t* hist, uint32_t* hist_full, float sigma_fixed) {

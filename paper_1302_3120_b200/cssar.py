@@ -30,6 +30,7 @@ SYMBOLS = [
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
+CSSAR_FLAG_ADAPTIVE_MU = 2
 STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
 
 
@@ -52,7 +53,7 @@ class ItaParamsC(ctypes.Structure):
 
 class IterLogC(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_float), ("lam", ctypes.c_float), ("support", ctypes.c_int64),
-                ("resid2", ctypes.c_double)]
+                ("resid2", ctypes.c_double), ("mu", ctypes.c_float)]
 
 
 _lib = None
@@ -218,19 +219,24 @@ class Plan:
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
                     log=False, profile_stages=False, stream=None):
-        """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X."""
+        """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X.
+        mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU)."""
         if X is None:
             X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
+        adaptive = isinstance(mu, str)
+        if adaptive and mu != "adaptive":
+            raise ValueError("mu must be a positive number or 'adaptive'")
         prm = ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
-                         int(k), float(lam), float(mu), int(iters),
-                         CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0)
+                         int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
+                         (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
+                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0))
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
                                         logbuf if log else None, _stream(stream))
         _check(rc, "cssar_ita_iterate")
         if log:
-            entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2)
+            entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu)
                        for e in list(logbuf)[:iters]]
             return X, entries
         return X
@@ -329,6 +335,6 @@ class Group:
         _check(self.lib.cssar_group_ita_iterate(self.h, ys, ms, ctypes.byref(prm), xs, logbuf if log else None,
                                                 _stream(stream)), "cssar_group_ita_iterate")
         if log:
-            return [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2)
+            return [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu)
                     for e in list(logbuf)[:iters]]
         return None

@@ -232,3 +232,44 @@ def test_ita_fallback_only_when_window_misses():
     pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr, rule="k", k=cfg.k, iters=30)
     fb = pl.debug_fallbacks()
     assert 1 <= fb <= 10, fb
+
+
+@pytest.mark.parametrize("name,iters", [("c0", 30), ("c1", 40)])
+def test_ita_adaptive_step_matches_oracle(name, iters):
+    """NEXT-1: the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU) vs the oracle's adaptive_mu:
+    X after the run (rel-L2 <= 1e-3), identical support, mu_i and sigma_i logs within 1e-4."""
+    prob = problem(name)
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    olog = []
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=cfg.thr, rule="k", k=cfg.k, mu="adaptive",
+                 iters=iters, log=olog)
+    pl = _plan(cfg.params)
+    Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr, rule="k", k=cfg.k,
+                              mu="adaptive", iters=iters, log=True)
+    Xg = to_host(Xg)
+    assert rel_l2(Xg, Xo) <= TOL_ITA
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
+    mo = np.array([e["mu"] for e in olog])
+    mg = np.array([e["mu"] for e in glog])
+    assert mo[0] == 1.0 and mg[0] == 1.0                  # empty support of X_0
+    assert np.all(mg >= 1.0 - 1e-6)                       # G unitary => mu_i >= 1
+    assert np.max(np.abs(mg - mo) / mo) <= 1e-4
+    so = np.array([e["sigma"] for e in olog])
+    sg = np.array([e["sigma"] for e in glog])
+    assert np.max(np.abs(sg - so) / so) <= 1e-4
+
+
+def test_ita_adaptive_step_fixed_lambda():
+    prob = problem("c0")
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    olog = []
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr="soft", rule="lambda", lam=60.0, mu="adaptive",
+                 iters=15, log=olog)
+    pl = _plan(cfg.params)
+    Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr="soft", rule="lambda", lam=60.0,
+                              mu="adaptive", iters=15, log=True)
+    assert rel_l2(to_host(Xg), Xo) <= TOL_ITA
+    assert [e["support"] for e in glog] == [e["support"] for e in olog]
+    assert np.max(np.abs(np.array([e["mu"] for e in glog]) - np.array([e["mu"] for e in olog]))) <= 1e-4
