@@ -58,7 +58,16 @@ typedef struct {
   int64_t n_az, n_rg;
 } cssar_sar_params;
 
-typedef enum { CSSAR_THR_SOFT = 1 /* q = 1, eq. 9 */, CSSAR_THR_HALF = 2 /* q = 1/2 */ } cssar_thr;
+/* thresholds E_sigma (eq. 7-9; P:L102 names q = 0, 1/2, 2/3, 1 as the analytic
+ * cases): soft q = 1 (eq. 9), half q = 1/2 (the north star's two), and (NEXT-4) hard q = 0
+ * and q = 2/3; all phase preserving with strict survival |b| > sigma.  Fixed-lambda jump
+ * points sigma(lambda mu): lm, (54^(1/3)/4) lm^(2/3), sqrt(lm), (2/3)(3 lm^3)^(1/4). */
+typedef enum {
+  CSSAR_THR_SOFT = 1,
+  CSSAR_THR_HALF = 2,
+  CSSAR_THR_HARD = 3,
+  CSSAR_THR_TWOTHIRDS = 4
+} cssar_thr;
 typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 /* eq. 7 */ } cssar_rule;
 
 /* flags: CSSAR_FLAG_PROFILE_STAGES launches the iteration body directly (no graph) with CUDA

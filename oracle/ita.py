@@ -22,6 +22,8 @@ Passages followed:
     normalised-IHT form of the cited source is used; mu_i = 1 when the support is empty or
     the denominator vanishes (S:L353).  With the k-rule sigma_i = |b|_(k+1) of b = X + mu_i dX;
     with a fixed lambda sigma_i = lambda mu_i (soft) / the half jump point of lambda mu_i.
+  * q = 0 (hard) and q = 2/3 thresholds (NEXT-4; P:L102 lists q = 0, 1/2, 2/3, 1 as the
+    analytic cases): hard keeps |b| > sigma; 2/3 is the closed-form L2/3 minimiser (twothirds).
 """
 import numpy as np
 
@@ -54,6 +56,39 @@ def half(b, sigma):
     return out
 
 
+def hard(b, sigma):
+    """q = 0 (NEXT-4; "analytically specified when q = 0"): keep b where |b| > sigma.
+    Penalty lambda mu ||x||_0 in the convention of the half operator: sigma = sqrt(lambda mu)."""
+    b = np.asarray(b, dtype=np.complex128)
+    return np.where(np.abs(b) > sigma, b, 0.0)
+
+
+def twothirds_lm_from_sigma(sigma):
+    """lambda mu whose L2/3 jump point (2/3)(3 (lambda mu)^3)^(1/4) equals sigma."""
+    return ((1.5 * sigma) ** 4 / 3.0) ** (1.0 / 3.0)
+
+
+def twothirds(b, sigma):
+    """q = 2/3 (NEXT-4): the closed-form minimiser of (x - t)^2 + lm |x|^(2/3) (the
+    L2/3 thresholding of the cited Lq theory), t = |b|, phase preserved, in the k-rule form
+    with lm = twothirds_lm_from_sigma(sigma):  for t > sigma
+      psi = arccosh(27 t^2 / (16 lm^(3/2))),  phi = (2/sqrt(3)) lm^(1/4) sqrt(cosh(psi/3)),
+      x = ((phi + sqrt(2 t / phi - phi^2)) / 2)^3."""
+    b = np.asarray(b, dtype=np.complex128)
+    if sigma == 0.0:
+        return b.copy()
+    a = np.abs(b)
+    out = np.zeros_like(b)
+    keep = a > sigma
+    t = a[keep]
+    lm = twothirds_lm_from_sigma(sigma)
+    psi = np.arccosh(27.0 * t ** 2 / (16.0 * lm ** 1.5))
+    phi = (2.0 / np.sqrt(3.0)) * lm ** 0.25 * np.sqrt(np.cosh(psi / 3.0))
+    mag = ((phi + np.sqrt(2.0 * t / phi - phi ** 2)) / 2.0) ** 3
+    out[keep] = b[keep] / t * mag
+    return out
+
+
 def half_sigma_from_lm(lm):
     """Jump point of half thresholding for penalty weight lambda*mu: (54^(1/3)/4)(lambda mu)^(2/3)."""
     return (54.0 ** (1.0 / 3.0) / 4.0) * lm ** (2.0 / 3.0)
@@ -74,12 +109,29 @@ def sigma_k_rule(b, k):
 
 
 def threshold(b, sigma, thr):
-    return soft(b, sigma) if thr == "soft" else half(b, sigma)
+    return {"soft": soft, "half": half, "hard": hard, "twothirds": twothirds}[thr](b, sigma)
 
 
 def sigma_fixed_lambda(lam, mu, thr):
     lm = lam * mu
-    return lm if thr == "soft" else half_sigma_from_lm(lm)
+    if thr == "soft":
+        return lm
+    if thr == "half":
+        return half_sigma_from_lm(lm)
+    if thr == "hard":
+        return np.sqrt(lm)
+    return (2.0 / 3.0) * (3.0 * lm ** 3) ** 0.25
+
+
+def lambda_from_sigma(sigma, mu, thr):
+    """lambda_i = the penalty weight whose threshold is sigma_i, divided by mu_i."""
+    if thr == "soft":
+        return sigma / mu
+    if thr == "half":
+        return HALF_LM_PER_SIGMA32 * sigma ** 1.5 / mu
+    if thr == "hard":
+        return sigma ** 2 / mu
+    return twothirds_lm_from_sigma(sigma) / mu
 
 
 def adaptive_mu(op, dX, X, mask):
@@ -118,8 +170,7 @@ def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10
             a = np.sort(np.abs(b).reshape(-1))[::-1]
             entry = dict(sigma=float(sigma), mu=float(mu_i), support=int(np.count_nonzero(Xn)),
                          resid2=float(np.vdot(R, R).real))
-            entry["lam"] = (float(sigma / mu_i) if thr == "soft"
-                            else float(HALF_LM_PER_SIGMA32 * sigma ** 1.5 / mu_i))
+            entry["lam"] = float(lambda_from_sigma(sigma, mu_i, thr))
             if rule == "k":
                 entry["gap"] = float((a[k - 1] - a[k]) / a[k]) if a[k] > 0 else float("inf")
             log.append(entry)

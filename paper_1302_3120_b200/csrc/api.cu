@@ -332,6 +332,8 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
 double fixed_sigma(const cssar_ita_params& prm) {
   const double lm = prm.lambda * prm.mu;
   if (prm.thr == CSSAR_THR_SOFT) return lm;
+  if (prm.thr == CSSAR_THR_HARD) return std::sqrt(lm);
+  if (prm.thr == CSSAR_THR_TWOTHIRDS) return (2.0 / 3.0) * std::pow(3.0 * lm * lm * lm, 0.25);
   return std::cbrt(54.0) / 4.0 * std::pow(lm, 2.0 / 3.0);
 }
 
@@ -589,7 +591,7 @@ int final_multi(const Ranks& R, const cssar_ita_params& prm, void* const* X, cud
 }
 
 int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
-  if (prm->thr != CSSAR_THR_SOFT && prm->thr != CSSAR_THR_HALF) return CSSAR_ERR_INVALID_PARAMS;
+  if (prm->thr < CSSAR_THR_SOFT || prm->thr > CSSAR_THR_TWOTHIRDS) return CSSAR_ERR_INVALID_PARAMS;
   if (prm->rule != CSSAR_RULE_KSPARSE && prm->rule != CSSAR_RULE_FIXED_LAMBDA) return CSSAR_ERR_INVALID_PARAMS;
   if (!(prm->mu > 0.0) || !std::isfinite(prm->mu)) return CSSAR_ERR_BAD_MU;
   if (prm->rule == CSSAR_RULE_KSPARSE && (prm->k < 1 || prm->k >= pl->n)) return CSSAR_ERR_BAD_K;

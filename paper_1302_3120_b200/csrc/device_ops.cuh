@@ -24,13 +24,24 @@ CSSAR_DEV uint32_t mag2_bits(float2 v) {
 }
 
 // E(b; sigma): strict survival on the fp32 |b|^2 pattern,
-// soft (eq. 9) or half (q = 1/2) shrink of the magnitude, phase preserved.
+// soft (eq. 9), half (q = 1/2), hard (q = 0) or q = 2/3 shrink of the magnitude, phase kept.
 CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
   const uint32_t u = mag2_bits(b);
   const float a2 = __uint_as_float(u);
   float f;
   if (thr == THR_SOFT) {
     f = fmaf(-sigma, rsqrtf(a2), 1.0f);                   // 1 - sigma/|b|   (sigma = 0 -> 1)
+  } else if (thr == THR_HARD) {
+    f = 1.0f;
+  } else if (thr == THR_TWOTHIRDS) {
+    // closed-form L2/3 minimiser in k-rule form (oracle/ita.py twothirds): q = 27 t^2 /
+    // (16 lm^(3/2)) = (3 sqrt(3)/4)(t/sigma)^2, phi = c sigma^(1/3) sqrt(cosh(acosh(q)/3))
+    const float t = a2 * rsqrtf(a2);
+    const float q = 1.2990381056766580f * a2 / (sigma * sigma);
+    const float phi = 1.2061639667263164f * cbrtf(sigma) * sqrtf(coshf(acoshf(q) * (1.0f / 3.0f)));
+    const float x = 0.5f * (phi + sqrtf(2.0f * t / phi - phi * phi));
+    f = x * x * x / t;
+    f = sigma == 0.f ? 1.0f : f;
   } else {
     const float ratio = sigma * rsqrtf(a2);
     const float phi = acosf(0.70710678118654752f * ratio * sqrtf(ratio));

@@ -12,7 +12,7 @@ namespace cssar {
 //   q[2] = Phi3 (azimuth compr. + residual) in u = j - n_rg/2
 struct RowCoef { Quad q[3]; };
 
-enum Thr : int { THR_SOFT = 1, THR_HALF = 2 };
+enum Thr : int { THR_SOFT = 1, THR_HALF = 2, THR_HARD = 3, THR_TWOTHIRDS = 4 };
 enum Rule : int { RULE_K = 1, RULE_LAMBDA = 2 };
 
 constexpr int HIST_BITS = 11;                  // top bits of the 31-bit |b|^2 pattern

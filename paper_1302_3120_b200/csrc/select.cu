@@ -206,6 +206,14 @@ __global__ void __launch_bounds__(512) fb_collect_kernel(const float2* __restric
   }
 }
 
+// lambda_i of a threshold sigma: the penalty weight whose jump point is sigma, / mu
+CSSAR_DEV float lambda_of_sigma(float sig, float mu, int thr) {
+  if (thr == THR_SOFT) return sig / mu;
+  if (thr == THR_HALF) return (float)(1.0886621079036347 * pow((double)sig, 1.5) / mu);
+  if (thr == THR_HARD) return sig * sig / mu;
+  return (float)(cbrt(pow(1.5 * (double)sig, 4.0) / 3.0) / mu);
+}
+
 // sigma^2 found: state for the next iteration (new sigma, histogram floor, candidate window,
 // log entry, counter resets).  Runs in thread 0 (bookkeeping) and all threads (resets).
 CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float mu, SelState* st, uint32_t* hist,
@@ -221,7 +229,7 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
       e.sigma = sig;
       const float m = st->mu > 0.f ? st->mu : mu;          // adaptive step of this iteration
       e.mu = m;
-      e.lam = thr == THR_SOFT ? sig / m : (float)(1.0886621079036347 * pow((double)sig, 1.5) / m);
+      e.lam = lambda_of_sigma(sig, m, thr);
       e.support = (long long)abv;
       e.resid2 = st->resid2;
       log[it] = e;
@@ -341,8 +349,7 @@ __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* 
     IterLogDev e;
     e.sigma = st->sigma_fixed;
     e.mu = m;
-    e.lam = thr == THR_SOFT ? st->sigma_fixed / m
-                            : (float)(1.0886621079036347 * pow((double)st->sigma_fixed, 1.5) / m);
+    e.lam = lambda_of_sigma(st->sigma_fixed, m, thr);
     e.support = (long long)st->support_fixed;
     e.resid2 = st->resid2;
     log[it] = e;

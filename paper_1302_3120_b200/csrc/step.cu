@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(512) adaptive_step_kernel(const AzArgs a, long
   float sf = 0.f;
   if (a.rule == RULE_LAMBDA) {
     const float lm = a.lambda * mu;
-    sf = a.thr == THR_SOFT ? lm : 0.94494078742115480f * powf(lm, 2.0f / 3.0f);   // (54^(1/3)/4)(lambda mu)^(2/3)
+    sf = a.thr == THR_SOFT   ? lm
+       : a.thr == THR_HALF   ? 0.94494078742115480f * powf(lm, 2.0f / 3.0f)   // (54^(1/3)/4)(lambda mu)^(2/3)
+       : a.thr == THR_HARD   ? sqrtf(lm)
+                             : (2.0f / 3.0f) * sqrtf(sqrtf(3.0f * lm * lm * lm));   // (2/3)(3 (lambda mu)^3)^(1/4)
     tc.s2fixed = __float_as_uint(__fmul_rn(sf, sf));
   }
   if (blockIdx.x == 0 && t == 0) {

@@ -12,7 +12,8 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcssar.so")
 
-CSSAR_THR_SOFT, CSSAR_THR_HALF = 1, 2
+CSSAR_THR_SOFT, CSSAR_THR_HALF, CSSAR_THR_HARD, CSSAR_THR_TWOTHIRDS = 1, 2, 3, 4
+THR_CODES = {"soft": 1, "half": 2, "hard": 3, "twothirds": 4}
 CSSAR_RULE_KSPARSE, CSSAR_RULE_FIXED_LAMBDA = 1, 2
 
 ERRORS = {
@@ -226,7 +227,7 @@ class Plan:
         adaptive = isinstance(mu, str)
         if adaptive and mu != "adaptive":
             raise ValueError("mu must be a positive number or 'adaptive'")
-        prm = ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
+        prm = ItaParamsC(THR_CODES[thr],
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
                          int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
                          (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
@@ -283,7 +284,7 @@ class Plan:
 
 
 def _itaprm(thr, rule, k, lam, mu, iters, profile_stages=False):
-    return ItaParamsC(CSSAR_THR_SOFT if thr == "soft" else CSSAR_THR_HALF,
+    return ItaParamsC(THR_CODES[thr],
                       CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
                       int(k), float(lam), float(mu), int(iters),
                       CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0)

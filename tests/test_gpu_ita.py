@@ -273,3 +273,43 @@ def test_ita_adaptive_step_fixed_lambda():
     assert rel_l2(to_host(Xg), Xo) <= TOL_ITA
     assert [e["support"] for e in glog] == [e["support"] for e in olog]
     assert np.max(np.abs(np.array([e["mu"] for e in glog]) - np.array([e["mu"] for e in olog]))) <= 1e-4
+
+
+@pytest.mark.parametrize("name,thr,iters", [("c0", "hard", 30), ("c1", "hard", 40), ("c0", "twothirds", 30),
+                                            ("c1", "twothirds", 40)])
+def test_ita_q0_and_q23_thresholds(name, thr, iters):
+    """NEXT-4: hard (q = 0) and q = 2/3 thresholds, k-rule, vs the oracle: X (rel-L2), support,
+    sigma logs; hard keeps exactly k pixels when no ties."""
+    prob = problem(name)
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    olog = []
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=thr, rule="k", k=cfg.k, iters=iters, log=olog)
+    pl = _plan(cfg.params)
+    Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=thr, rule="k", k=cfg.k, iters=iters,
+                              log=True)
+    Xg = to_host(Xg)
+    assert rel_l2(Xg, Xo) <= TOL_ITA
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
+    so = np.array([e["sigma"] for e in olog])
+    sg = np.array([e["sigma"] for e in glog])
+    assert np.max(np.abs(sg - so) / so) <= 1e-4
+    lo = np.array([e["lam"] for e in olog])
+    lg = np.array([e["lam"] for e in glog])
+    assert np.max(np.abs(lg - lo) / lo) <= 1e-3
+    if thr == "hard":
+        assert np.count_nonzero(Xg) == cfg.k
+
+
+def test_ita_fixed_lambda_hard_and_twothirds():
+    prob = problem("c0")
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    for thr, lam in (("hard", 3000.0), ("twothirds", 400.0)):
+        olog = []
+        Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=thr, rule="lambda", lam=lam, iters=15, log=olog)
+        pl = _plan(cfg.params)
+        Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=thr, rule="lambda", lam=lam,
+                                  iters=15, log=True)
+        assert rel_l2(to_host(Xg), Xo) <= TOL_ITA, thr
+        assert [e["support"] for e in glog] == [e["support"] for e in olog], thr

@@ -232,3 +232,36 @@ def test_adaptive_ita_equals_fixed_step_at_full_sampling():
     Xf = ita.ita(op, Y, full, thr="soft", rule="k", k=cfg.k, mu=1.0, iters=4)
     assert all(abs(e["mu"] - 1.0) <= 1e-12 for e in log)
     assert np.max(np.abs(Xa - Xf)) <= 1e-12 * np.max(np.abs(Xf))
+
+
+# ---------------------------------------------------------------- q = 0 and q = 2/3 (NEXT-4)
+def test_hard_threshold_keeps_exactly_the_top_k():
+    b = _rand(4000, 11)
+    k = 137
+    sig = ita.sigma_k_rule(b, k)
+    X = ita.hard(b, sig)
+    assert np.count_nonzero(X) == k
+    keep = np.argsort(-np.abs(b))[:k]
+    assert np.array_equal(X[keep], b[keep])
+    assert np.array_equal(ita.hard(b, 0.0), b)
+
+
+def test_twothirds_matches_bruteforce_minimiser():
+    """argmin_{x>=0} (x - t)^2 + lm x^(2/3) by a dense grid, lm from the k-rule sigma."""
+    for sigma in (0.3, 1.0, 2.5):
+        lm = ita.twothirds_lm_from_sigma(sigma)
+        assert abs((2.0 / 3.0) * (3.0 * lm ** 3) ** 0.25 - sigma) <= 1e-12 * sigma
+        for t in (0.9 * sigma, 1.0001 * sigma, 1.3 * sigma, 2.0 * sigma, 6.0 * sigma):
+            x = np.linspace(0.0, 2.0 * t, 400001)
+            ref = x[np.argmin((x - t) ** 2 + lm * x ** (2.0 / 3.0))]
+            got = abs(ita.twothirds(np.array([t * np.exp(0.3j)]), sigma)[0])
+            assert abs(got - ref) <= 2.0 * (x[1] - x[0]) + 1e-12, (sigma, t, got, ref)
+
+
+def test_twothirds_jump_phase_and_identity():
+    sigma = 1.7
+    b = np.array([sigma * (1 + 1e-9) * np.exp(1.1j), 0.5 * sigma * np.exp(-2j)])
+    X = ita.twothirds(b, sigma)
+    assert abs(abs(X[0]) - sigma / 2.0) <= 1e-6 * sigma           # jumps from 0 to sigma/2
+    assert abs(np.angle(X[0]) - 1.1) <= 1e-12 and X[1] == 0
+    assert np.array_equal(ita.twothirds(b, 0.0), b)
