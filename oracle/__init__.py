@@ -7,6 +7,7 @@ headers, helpers, tables or constant generators.
 
 Modules (each function cites the PAPER.md passage it follows):
   csa      CSA focusing M and approximated observation G = M^H (eq. 10-11, Theorem 1)
+  rda      RDA focusing M and G = M^H with the truncated-sinc RCMC and its transpose (eq. 14-18, 23)
   ita      soft / half thresholds, k-rule and fixed-lambda rules, Algorithm 1 (eq. 7-9, 25-28)
   echo     exact periodic point-target echo (eq. 1-3) and inverse-CSA echo
   metrics  IRW / PSLR of a focused point target (P:L512 method)
@@ -22,4 +23,4 @@ Parity unpinned: whether this CSA chain is the operator the paper in
 tests, not by paper values; the L1/2 operator constants (not printed at P:L102) — pinned
 by brute-force minimisation of its defining objective.
 """
-from . import csa, ita, echo, metrics  # noqa: F401
+from . import csa, ita, echo, metrics, rda  # noqa: F401
