@@ -56,7 +56,18 @@ enum {
 typedef struct {
   double fc, Kr, Tr, Fr, prf, Vr, R_ref, squint;
   int64_t n_az, n_rg;
+  int32_t op;       /* cssar_op: the approximated observation pair (0 = CSSAR_OP_CSA) */
 } cssar_sar_params;
+
+/* The focusing method M whose inverse is the approximated observation G = M^H:
+ *   CSSAR_OP_CSA (north star): chirp scaling, M = F_eta^-1 Phi3 F_tau^-1 Phi2 F_tau Phi1 F_eta.
+ *   CSSAR_OP_RDA (NEXT-2, the paper's own CSRDA, eq. 14-18, 23): range-Doppler,
+ *     M = F_eta^-1 P_eta C F_tau^-1 P_tau F_tau F_eta with the 8-tap truncated-sinc RCMC C
+ *     (space-variant shift R0 (1/D - 1), torus indices) and G = M^H with D = C^T.
+ *     Requires (1/D_max - 1) n_rg < 1/2 at the Doppler edge (else CSSAR_ERR_INVALID_PARAMS).
+ * Every call (operators, ITA, world > 1) uses the plan's pair; the sweeps are the same except
+ * the range sweep, which carries the RCMC. */
+typedef enum { CSSAR_OP_CSA = 1, CSSAR_OP_RDA = 2 } cssar_op;
 
 /* thresholds E_sigma (eq. 7-9; P:L102 names q = 0, 1/2, 2/3, 1 as the analytic
  * cases): soft q = 1 (eq. 9), half q = 1/2 (the north star's two), and (NEXT-4) hard q = 0

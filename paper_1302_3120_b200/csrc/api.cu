@@ -44,6 +44,7 @@ struct cssar_plan_s {
   int sm_count = 148;
   RowCoef* d_coef = nullptr;
   float2* d_rg_tab = nullptr;     // phase exp table + range-engine twiddles
+  float2* d_rcmc = nullptr;       // RDA plans: per-row RCMC migration (alpha, s0); CSA: nullptr
   float2* d_az_tab = nullptr;     // azimuth-engine twiddles (head / tail / operator kernels)
   float2* d_az_tab_r = nullptr;   // azimuth-engine twiddles (residual kernel)
   SelState* d_st = nullptr;
@@ -144,6 +145,36 @@ std::vector<RowCoef> build_coefficients(const cssar_sar_params& p) {
   return tab;
 }
 
+// NEXT-2 RDA operator pair (oracle/rda.py; eq. 14-18, 23): per Doppler bin i
+//   q[1] = P_tau = exp(+j pi f_tau^2 / K_r)      cycles (1/(2 K_r)) (F_r/N)^2 l'^2
+//   q[2] = P_eta = exp(-j pi f^2 / K_a(R0) + j 4 pi fc R0 / c),  K_a = 2 V_r^2 fc / (c R0),
+//          R0 = R_ref + u c / (2 F_r):  cycles -(f^2 c R_ref)/(4 V_r^2 fc) + 2 fc R_ref / c
+//          + u (fc / F_r - f^2 c^2 / (8 V_r^2 fc F_r))
+//   rcmc = (alpha, s0): migration d = R0 (1/D - 1) 2 F_r / c = s0 + alpha u range cells,
+//          alpha = 1/D - 1, s0 = alpha 2 R_ref F_r / c   (u = j - N/2)
+std::vector<RowCoef> build_coefficients_rda(const cssar_sar_params& p, std::vector<float2>& rcmc) {
+  const long long na = p.n_az, nr = p.n_rg;
+  std::vector<RowCoef> tab((size_t)na);
+  rcmc.assign((size_t)na, float2{0.f, 0.f});
+  const long double fc = p.fc, Kr = p.Kr, Fr = p.Fr, prf = p.prf, Vr = p.Vr, Rr = p.R_ref;
+  const long double df = Fr / (long double)nr;
+  for (long long i = 0; i < na; ++i) {
+    const long long is = (i < (na + 1) / 2) ? i : i - na;
+    const long double f = (long double)is * prf / (long double)na;
+    const long double xr = kC * f / (2.0L * Vr * fc);
+    const long double x = xr * xr;
+    const long double D = sqrtl(1.0L - x);
+    const long double idm1 = (x / (1.0L + D)) / D;
+    RowCoef rc{};
+    rc.q[1] = {frac_u64(df * df / (2.0L * Kr)), 0ull, 0ull};
+    rc.q[2] = {0ull, frac_u64(fc / Fr - f * f * kC * kC / (8.0L * Vr * Vr * fc * Fr)),
+               frac_u64(2.0L * fc * Rr / kC - f * f * kC * Rr / (4.0L * Vr * Vr * fc))};
+    tab[(size_t)i] = rc;
+    rcmc[(size_t)i] = float2{(float)idm1, (float)(idm1 * 2.0L * Rr * Fr / kC)};
+  }
+  return tab;
+}
+
 int validate_params(const cssar_sar_params& p) {
   if (!(p.fc > 0 && p.Kr > 0 && p.Tr > 0 && p.Fr > 0 && p.prf > 0 && p.Vr > 0 && p.R_ref > 0))
     return CSSAR_ERR_INVALID_PARAMS;
@@ -157,6 +188,14 @@ int validate_params(const cssar_sar_params& p) {
   if (299792458.0 * fmax / (2.0 * p.Vr * p.fc) >= 1.0) return CSSAR_ERR_INVALID_PARAMS;
   const int la = ilog2_exact(p.n_az), lr = ilog2_exact(p.n_rg);
   if (la < 7 || la > 15 || lr < 7 || lr > 14) return CSSAR_ERR_UNSUPPORTED_SIZE;
+  if (p.op != 0 && p.op != CSSAR_OP_CSA && p.op != CSSAR_OP_RDA) return CSSAR_ERR_INVALID_PARAMS;
+  if (p.op == CSSAR_OP_RDA) {
+    // the RCMC transpose gathers from a fixed window: the migration may vary by < 1/2 cell
+    // across the row at the Doppler edge (alpha n_rg < 1/2)
+    const double xr = 299792458.0 * fmax / (2.0 * p.Vr * p.fc);
+    const double D = std::sqrt(1.0 - xr * xr);
+    if ((1.0 / D - 1.0) * (double)p.n_rg >= 0.5) return CSSAR_ERR_INVALID_PARAMS;
+  }
   return CSSAR_OK;
 }
 
@@ -236,6 +275,7 @@ int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yo
   a.out = (float2*)Yout;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_PLAIN, a.n_rg, a, s));
   RgArgs r{(float2*)Yout, pl->d_coef, 0, pl->d_rg_tab};
+  r.rcmc = pl->d_rcmc;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Yout;
   a.mask = mask;
@@ -255,6 +295,7 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
   a.mask = mask;
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_MASK, a.n_rg, a, s));
   RgArgs r{(float2*)Xout, pl->d_coef, 0, pl->d_rg_tab};
+  r.rcmc = pl->d_rcmc;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Xout;
   a.mask = nullptr;
@@ -283,6 +324,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.mask = mask;
   float2* b = (float2*)X;
   RgArgs r{pl->U, pl->d_coef, 0, pl->d_rg_tab};
+  r.rcmc = pl->d_rcmc;
   MARK(0);
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
   a.in = b;
@@ -413,6 +455,7 @@ AzArgs az_col_args(cssar_plan pl, const cssar_ita_params& prm) {
 
 RgArgs rg_row_args(cssar_plan pl) {
   RgArgs r{pl->Vrow, pl->d_coef, (int)(pl->rank * pl->nrow), pl->d_rg_tab, 0, 0};
+  r.rcmc = pl->d_rcmc;
   r.log_w = ilog2_exact(pl->ncol);
   r.blk = pl->nrow * pl->ncol;
   return r;
@@ -787,7 +830,14 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev);
-  std::vector<RowCoef> tab = build_coefficients(*p);
+  std::vector<float2> rcmc;
+  std::vector<RowCoef> tab = p->op == CSSAR_OP_RDA ? build_coefficients_rda(*p, rcmc) : build_coefficients(*p);
+  if (!rcmc.empty() &&
+      (cudaMalloc(&pl->d_rcmc, sizeof(float2) * rcmc.size()) != cudaSuccess ||
+       cudaMemcpy(pl->d_rcmc, rcmc.data(), sizeof(float2) * rcmc.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+    cssar_plan_destroy(pl);
+    return CSSAR_ERR_CUDA;
+  }
   if (cudaMalloc(&pl->d_coef, sizeof(RowCoef) * tab.size()) != cudaSuccess ||
       cudaMemcpy(pl->d_coef, tab.data(), sizeof(RowCoef) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMalloc(&pl->d_st, sizeof(SelState)) != cudaSuccess ||
@@ -900,6 +950,7 @@ int cssar_plan_destroy(cssar_plan pl) {
     if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
   cudaFree(pl->d_coef);
   cudaFree(pl->d_rg_tab);
+  cudaFree(pl->d_rcmc);
   cudaFree(pl->d_az_tab);
   cudaFree(pl->d_az_tab_r);
   cudaFree(pl->d_st);
@@ -1093,6 +1144,7 @@ int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
   if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
   RgArgs r{(float2*)U, pl->d_coef, 0, pl->d_rg_tab};
+  r.rcmc = pl->d_rcmc;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody != 0, (int)pl->p.n_az, r, (cudaStream_t)stream));
   return CSSAR_OK;
 }

@@ -100,6 +100,9 @@ struct RgArgs {
   float2* dst[16];
   int dlog_nrow;
   int drank;
+  // RDA operator pair (NEXT-2; cssar_sar_params::op = CSSAR_OP_RDA): per global Doppler row
+  // (alpha, s0) of the RCMC migration d(j) = s0 + alpha (j - n_rg/2) range cells; nullptr = CSA
+  const float2* rcmc;
 };
 
 enum AzMode : int {

@@ -20,9 +20,79 @@ struct RgCfg {
   static constexpr size_t SMEM = sizeof(float2) * (N * B + TAB);
 };
 
+// ------------------------------------------------------------------ RDA RCMC (NEXT-2)
+// eq. 16 with the truncated kernel of 8 taps on the torus (oracle/rda.py):
+// output gate j of Doppler row i sits at j + d(j), d(j) = s0_i + alpha_i (j - N/2) range cells
+// (alpha = 1/D - 1, s0 = alpha 2 R_ref F_r / c), taps m = floor(d) - 3 .. floor(d) + 4:
+//   C   : U[j] = sum_m sinc(m - d(j)) V[(j + m) mod N]
+//   D=C^T (eq. 17, 23): W[k] = sum_{j, m : j + m = k mod N} sinc(m - d(j)) V[j]
+// with sinc(m - d) = (-1)^(m+1) sin(pi d) / (pi (m - d)) (= 1 at m = d, d an integer).
+CSSAR_DEV float rcmc_shift(float2 rc, int j, int n) { return fmaf(rc.x, (float)(j - n / 2), rc.y); }
+
+// C at output gate j of one row staged (unswizzled) in SMEM row v
+template <int N>
+CSSAR_DEV float2 rcmc_gather(const float2* v, float2 rc, int j) {
+  const float d = rcmc_shift(rc, j, N);
+  const float fl = floorf(d);
+  const float S = sinpif(d) * 0.318309886183790672f;       // sin(pi d) / pi
+  const int m0 = (int)fl - 3;
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int m = m0 + t;
+    const float den = (float)m - d;
+    const float w = den == 0.f ? 1.0f : __fdividef((m & 1) ? S : -S, den);
+    const float2 x = v[(j + m) & (N - 1)];
+    acc.x = fmaf(w, x.x, acc.x);
+    acc.y = fmaf(w, x.y, acc.y);
+  }
+  return acc;
+}
+
+// S(d) V for the transpose: V premultiplied by sin(pi d(j)) / pi, or V itself where d(j) is an
+// integer (the kernel is then the unit impulse at m = d)
+template <int N>
+CSSAR_DEV float2 rcmc_stage_T(float2 x, float2 rc, int j) {
+  const float d = rcmc_shift(rc, j, N);
+  const float S = d == floorf(d) ? 1.0f : sinpif(d) * 0.318309886183790672f;
+  return make_float2(S * x.x, S * x.y);
+}
+
+// D = C^T at output gate k: the sources j' = k - m whose 8 taps cover k; |d(j) - d(k)| < 1
+// for every j of the row (validated at plan creation: alpha n_rg < 1/2), so they lie in
+// j' = k - floor(d(k)) - 5 .. k - floor(d(k)) + 4 (unwrapped; j = j' mod N)
+template <int N>
+CSSAR_DEV float2 rcmc_scatter_T(const float2* p, float2 rc, int k) {
+  const int jc = k - (int)floorf(rcmc_shift(rc, k, N));
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = -5; c < 5; ++c) {
+    const int jp = jc + c;
+    const int j = jp & (N - 1);
+    const float d = rcmc_shift(rc, j, N);
+    const float fl = floorf(d);
+    const int m = k - jp;
+    const int mm = m - (int)fl;
+    if (mm >= -3 && mm <= 4) {
+      float w;
+      if (d == fl) {
+        w = mm == 0 ? 1.0f : 0.0f;
+      } else {
+        w = __fdividef((m & 1) ? 1.0f : -1.0f, (float)m - d);
+      }
+      const float2 x = p[j];
+      acc.x = fmaf(w, x.x, acc.x);
+      acc.y = fmaf(w, x.y, acc.y);
+    }
+  }
+  return acc;
+}
+
 // GBODY: Phi3* -> F -> Phi2* -> F^-1 -> Phi1*  (inverse of the focusing steps)
 // else : Phi1  -> F -> Phi2  -> F^-1 -> Phi3   (CSA focusing body)
-template <int LOGN, bool GBODY, bool BLK>
+// RDA  : GBODY P_eta* -> D -> F -> P_tau* -> F^-1 ; else F -> P_tau -> F^-1 -> C -> P_eta
+//        (eq. 14 / eq. 18 between the azimuth DFTs; q[1] = P_tau, q[2] = P_eta)
+template <int LOGN, bool GBODY, bool BLK, bool RDA>
 __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_kernel(const RgArgs a) {
   using C = RgCfg<LOGN>;
   using En = typename C::En;
@@ -55,10 +125,26 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   });
   cp_async_wait_all();
   __syncthreads();                                                        // tables visible
-  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // prologue phase
-    const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
-    phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
-  });
+  if constexpr (!RDA) {
+    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // prologue phase
+      const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
+      phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
+    });
+  } else if constexpr (GBODY) {
+    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage S V
+      const int row = a.row_base + row0 + b;
+      phase_apply<R0, N / R0, true>(tab, a.coef[row].q[2], j - N / 2, x);
+      const float2 rc = a.rcmc[row];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) s[b * N + j + r * (N / R0)] = rcmc_stage_T<N>(x[r], rc, j + r * (N / R0));
+    });
+    __syncthreads();
+    En::template for_groups<LR0>(v, t, [&](int b, int k, float2* x) {    // D = C^T
+      const float2 rc = a.rcmc[a.row_base + row0 + b];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = rcmc_scatter_T<N>(s + b * N, rc, k + r * (N / R0));
+    });                                 // the FFT's first exchange syncs before overwriting s
+  }
   En::template passes_from<-1, false, 0>(s, v, t, tw);                   // range FFT
   En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
     const Quad q = a.coef[a.row_base + row0 + b].q[1];
@@ -67,9 +153,26 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
   });
   En::template passes_from<+1, true, 0>(s, v, t, tw);                    // range IFFT
+  if constexpr (RDA && !GBODY) {                                          // C on the whole row
+    __syncthreads();                    // every thread finished reading the last exchange
+    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) s[b * N + j + r * (N / R0)] = x[r];
+    });
+    __syncthreads();
+    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+      const float2 rc = a.rcmc[a.row_base + row0 + b];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = rcmc_gather<N>(s + b * N, rc, j + r * (N / R0));
+    });
+  }
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
-    const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
-    phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
+    if constexpr (!RDA) {
+      const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
+      phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
+    } else if constexpr (!GBODY) {
+      phase_apply<R0, N / R0, false>(tab, a.coef[a.row_base + row0 + b].q[2], j - N / 2, x);   // P_eta
+    }
     if constexpr (BLK) {
       if (a.dst[0]) {                      // fused transpose: straight into the ranks' column slabs
         const int wm = (1 << a.log_w) - 1;
@@ -124,7 +227,7 @@ cudaError_t rg_table_fill(int log_nrg, float2* dst, cudaStream_t s) {
 template <int LOGN, bool GB, bool BLK>
 static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
   using C = RgCfg<LOGN>;
-  auto k = rg_sweep_kernel<LOGN, GB, BLK>;
+  auto k = a.rcmc ? rg_sweep_kernel<LOGN, GB, BLK, true> : rg_sweep_kernel<LOGN, GB, BLK, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
   k<<<n_rows / C::B, C::T, C::SMEM, s>>>(a);

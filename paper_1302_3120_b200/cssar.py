@@ -43,7 +43,10 @@ class CssarError(RuntimeError):
 
 class SarParamsC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in ("fc", "Kr", "Tr", "Fr", "prf", "Vr", "R_ref", "squint")] + \
-               [("n_az", ctypes.c_int64), ("n_rg", ctypes.c_int64)]
+               [("n_az", ctypes.c_int64), ("n_rg", ctypes.c_int64), ("op", ctypes.c_int32)]
+
+
+OP_CODES = {"csa": 1, "rda": 2}   # cssar_op (include/cssar.h): the approximated observation pair
 
 
 class ItaParamsC(ctypes.Structure):
@@ -121,8 +124,9 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _params_c(p):
-    return SarParamsC(p.fc, p.Kr, p.Tr, p.Fr, p.prf, p.Vr, p.R_ref, p.squint, int(p.n_az), int(p.n_rg))
+def _params_c(p, op="csa"):
+    return SarParamsC(p.fc, p.Kr, p.Tr, p.Fr, p.prf, p.Vr, p.R_ref, p.squint, int(p.n_az), int(p.n_rg),
+                      OP_CODES[op])
 
 
 def nccl_unique_id():
@@ -152,16 +156,18 @@ def pack_mask(mask_u8, stream=None):
 class Plan:
     """cssar_plan: SAR parameters -> phase-coefficient table; operator calls and ITA."""
 
-    def __init__(self, params, stream=None, workspace=True, world=1, rank=0, unique_id=None):
+    def __init__(self, params, stream=None, workspace=True, world=1, rank=0, unique_id=None, op="csa"):
         """world > 1: this process is `rank` of a slab-partitioned plan; its
         arrays are row slabs of n_az/world azimuth lines; unique_id = the 128-byte NCCL id
-        (nccl_unique_id() on one rank, shared by the caller, e.g. dist.broadcast_object_list)."""
+        (nccl_unique_id() on one rank, shared by the caller, e.g. dist.broadcast_object_list).
+        op: "csa" (north star) or "rda" (NEXT-2, the paper's CSRDA pair, eq. 14-18)."""
         self.lib = load_library()
         self.params = params
+        self.op = op
         self.world, self.rank = int(world), int(rank)
         self.shape = (int(params.n_az) // self.world, int(params.n_rg))
         h = ctypes.c_void_p()
-        pc = _params_c(params)
+        pc = _params_c(params, op)
         uid = None
         if self.world > 1:
             if unique_id is None or len(unique_id) != 128:
@@ -294,13 +300,14 @@ class Group:
     """cssar_group: `world` rank plans emulated on the current device — the multi-GPU
     schedule (slab partition, transposes, reduced select) with device-copy exchanges."""
 
-    def __init__(self, params, world, stream=None):
+    def __init__(self, params, world, stream=None, op="csa"):
         self.lib = load_library()
         self.params = params
+        self.op = op
         self.world = int(world)
         self.shape = (int(params.n_az) // self.world, int(params.n_rg))
         h = ctypes.c_void_p()
-        pc = _params_c(params)
+        pc = _params_c(params, op)
         _check(self.lib.cssar_group_create(ctypes.byref(h), ctypes.byref(pc), self.world, _stream(stream)),
                "cssar_group_create")
         self.h = h

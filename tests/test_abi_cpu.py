@@ -68,3 +68,19 @@ def test_sm100a_code_in_library():
     lib = os.path.join(PKG, "libcssar.so")
     out = subprocess.run([cuobjdump, "--list-elf", lib], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_params_validation_without_gpu():
+    """cssar_plan_create validates before any CUDA call: operator code and the RDA window
+    bound (include/cssar.h cssar_op: (1/D_max - 1) n_rg < 1/2)."""
+    from inputs.configs import SarParams
+    from paper_1302_3120_b200 import cssar
+    lib = cssar.load_library()
+    h = ctypes.c_void_p()
+    bad_op = cssar._params_c(SarParams(n_az=256, n_rg=256))
+    bad_op.op = 7
+    assert lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(bad_op), 1, 0, None, None) == -1
+    # prf 4000 Hz at 16384 gates: the RDA migration varies by 0.53 cell across the row
+    wide = cssar._params_c(SarParams(n_az=256, n_rg=16384, Fr=120e6, prf=4000.0), "rda")
+    assert lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(wide), 1, 0, None, None) == -1
+    assert not h.value
