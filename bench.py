@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c3")
+    ap.add_argument("--op", default="csa", choices=["csa", "rda"],
+                    help="approximated observation pair (rda: NEXT-2, the paper's CSRDA; not the north star)")
     ap.add_argument("--impl", default="cssar", choices=["cssar", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -197,7 +199,7 @@ def main():
     cfg = configs.get(args.config)
     p = cfg.params
     n = p.n_az * p.n_rg
-    plan = Plan(p)
+    plan = Plan(p, op=args.op)
     Y, mb, mask, sc = make_problem_gpu(cfg, plan)
     X = torch.zeros_like(Y)
     kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
@@ -213,7 +215,7 @@ def main():
         X = torch.zeros_like(Y)
         del plan
         torch.cuda.synchronize()
-        plan = Plan(p, world=world, rank=rank, unique_id=uid[0])
+        plan = Plan(p, world=world, rank=rank, unique_id=uid[0], op=args.op)
     sampler = ClockSampler(local)
     sampler.start()
     plan.ita_iterate(Y, mb, X=X, iters=args.warmup, **kw)
@@ -264,7 +266,7 @@ def main():
         "ms_per_step": ms_step, "it_per_s": it_s, "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {p.n_az}x{p.n_rg} complex64, {cfg.scene} scene, {cfg.mask} mask "
+        "config": {"workload": f"{args.config}{'' if args.op == 'csa' else ' [RDA pair]'}: {p.n_az}x{p.n_rg} complex64, {cfg.scene} scene, {cfg.mask} mask "
                                f"{cfg.rate}, SNR {cfg.snr_db} dB, {cfg.thr} threshold, k = {cfg.k}, mu = {cfg.mu}",
                    "n_az": p.n_az, "n_rg": p.n_rg, "k": cfg.k, "l2": "inputs larger than L2 (512 MiB arrays)",
                    "parallelism": "single" if world == 1 else

@@ -195,6 +195,10 @@ int validate_params(const cssar_sar_params& p) {
     const double xr = 299792458.0 * fmax / (2.0 * p.Vr * p.fc);
     const double D = std::sqrt(1.0 - xr * xr);
     if ((1.0 / D - 1.0) * (double)p.n_rg >= 0.5) return CSSAR_ERR_INVALID_PARAMS;
+    // the wrap-around outputs of D recomputed exactly are those within 12 gates of the row
+    // start (rg.cu kRcmcWrapLo): the migration must stay below 6 cells
+    if ((1.0 / D - 1.0) * (2.0 * p.R_ref * p.Fr / 299792458.0 + 0.5 * (double)p.n_rg) >= 6.0)
+      return CSSAR_ERR_INVALID_PARAMS;
   }
   return CSSAR_OK;
 }

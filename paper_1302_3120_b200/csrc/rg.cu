@@ -1,4 +1,5 @@
 // Range sweeps (S2 G body, S4 M body): one or more range lines per CTA.
+#include <type_traits>
 #include "device_ops.cuh"
 #include "cluster.cuh"
 
@@ -23,64 +24,94 @@ struct RgCfg {
 // ------------------------------------------------------------------ RDA RCMC (NEXT-2)
 // eq. 16 with the truncated kernel of 8 taps on the torus (oracle/rda.py):
 // output gate j of Doppler row i sits at j + d(j), d(j) = s0_i + alpha_i (j - N/2) range cells
-// (alpha = 1/D - 1, s0 = alpha 2 R_ref F_r / c), taps m = floor(d) - 3 .. floor(d) + 4:
+// (alpha = 1/D - 1 >= 0, s0 = alpha 2 R_ref F_r / c), taps m = floor(d) - 3 .. floor(d) + 4:
 //   C   : U[j] = sum_m sinc(m - d(j)) V[(j + m) mod N]
 //   D=C^T (eq. 17, 23): W[k] = sum_{j, m : j + m = k mod N} sinc(m - d(j)) V[j]
-// with sinc(m - d) = (-1)^(m+1) sin(pi d) / (pi (m - d)) (= 1 at m = d, d an integer).
+// sinc(m - d) = (-1)^(m+1) sin(pi d) / (pi (m - d)) (= 1 at m = d).
+//
+// Evaluation: the row is staged in SMEM and every thread
+// produces 32 consecutive outputs from a sliding register window of 9 inputs.  d varies by
+// alpha <= 6e-6 cell per gate (alpha n_rg < 1/2, validated), so over a chunk's 64-gate bracket
+// each tap weight sinc(m - d(i)) is linear in the gate index i to < 6e-8: it is evaluated
+// exactly at the bracket ends and interpolated (one FMA per tap and output).  The union
+// window m = F - 3 .. F + 5 (F = floor d at the bracket start) covers the one possible integer
+// crossing of d inside the bracket; its end taps are switched by the crossing gate.  D outputs
+// whose sources wrap around the torus (d jumps by alpha n_rg there) are recomputed exactly.
 CSSAR_DEV float rcmc_shift(float2 rc, int j, int n) { return fmaf(rc.x, (float)(j - n / 2), rc.y); }
+CSSAR_DEV int rsw(int i) { return i ^ ((i >> 5) & 31); }        // staged-row swizzle
+constexpr float kInvPi = 0.318309886183790672f;
+constexpr int kRcmcWrapLo = 12, kRcmcWrapHi = 3;                  // D outputs recomputed exactly
 
-// C at output gate j of one row staged (unswizzled) in SMEM row v
-template <int N>
-CSSAR_DEV float2 rcmc_gather(const float2* v, float2 rc, int j) {
-  const float d = rcmc_shift(rc, j, N);
-  const float fl = floorf(d);
-  const float S = sinpif(d) * 0.318309886183790672f;       // sin(pi d) / pi
-  const int m0 = (int)fl - 3;
-  float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int m = m0 + t;
-    const float den = (float)m - d;
-    const float w = den == 0.f ? 1.0f : __fdividef((m & 1) ? S : -S, den);
-    const float2 x = v[(j + m) & (N - 1)];
-    acc.x = fmaf(w, x.x, acc.x);
-    acc.y = fmaf(w, x.y, acc.y);
+CSSAR_DEV float sinc_md(int m, float d, float sd) {                // sd = sin(pi d) / pi
+  const float den = (float)m - d;
+  return den == 0.f ? 1.0f : __fdividef((m & 1) ? sd : -sd, den);
+}
+
+// 32 consecutive outputs k0 .. k0+31 of C (TR = false) or D (TR = true) of one staged row
+template <int N, bool TR>
+CSSAR_DEV void rcmc_chunk(const float2* row, float2 rc, int k0, float2 (&out)[32]) {
+  const int ia = k0 - 16, ib = ia + 64;
+  const float da = rcmc_shift(rc, ia, N), db = rcmc_shift(rc, ib, N);
+  const int F = (int)floorf(da);
+  int brk = ib + 1;                                   // first gate with floor(d) = F + 1
+  if ((int)floorf(db) > F) {
+    int lo = ia, hi = ib;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)floorf(rcmc_shift(rc, mid, N)) > F) hi = mid; else lo = mid;
+    }
+    brk = hi;
   }
-  return acc;
+  const float sa = sinpif(da) * kInvPi, sb = sinpif(db) * kInvPi;
+  float A[9], S[9];
+#pragma unroll
+  for (int u = 0; u < 9; ++u) {
+    const int m = F - 3 + u;
+    const float ga = sinc_md(m, da, sa);
+    S[u] = (sinc_md(m, db, sb) - ga) * (1.0f / 64.0f);
+    // weight of tap u at output n: ga + (i - ia) S, i = the gate whose d it uses
+    A[u] = fmaf((float)(TR ? 19 - F - u : 16), S[u], ga);
+  }
+  const int n0 = TR ? brk - k0 + F - 3 : brk - k0;    // tap 0 only while n < n0
+  const int n8 = TR ? brk - k0 + F + 5 : brk - k0;    // tap 8 only once n >= n8
+  const int base = TR ? k0 - F - 5 : k0 + F - 3;
+  float2 win[9];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) win[q] = row[rsw((base + q) & (N - 1))];
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    win[8] = row[rsw((base + n + 8) & (N - 1))];
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      float w = fmaf(S[u], (float)n, A[u]);
+      if (u == 0) w = n < n0 ? w : 0.0f;
+      if (u == 8) w = n >= n8 ? w : 0.0f;
+      const float2 x = win[TR ? 8 - u : u];
+      acc.x = fmaf(w, x.x, acc.x);
+      acc.y = fmaf(w, x.y, acc.y);
+    }
+    out[n] = acc;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) win[q] = win[q + 1];
+  }
 }
 
-// S(d) V for the transpose: V premultiplied by sin(pi d(j)) / pi, or V itself where d(j) is an
-// integer (the kernel is then the unit impulse at m = d)
+// D at output k, exact: the sources j' = k - m whose 8 taps cover k; |d(j) - d(k)| < 1 for
+// every gate of the row, so they lie in j' = k - floor(d(k)) - 5 .. + 4 (unwrapped)
 template <int N>
-CSSAR_DEV float2 rcmc_stage_T(float2 x, float2 rc, int j) {
-  const float d = rcmc_shift(rc, j, N);
-  const float S = d == floorf(d) ? 1.0f : sinpif(d) * 0.318309886183790672f;
-  return make_float2(S * x.x, S * x.y);
-}
-
-// D = C^T at output gate k: the sources j' = k - m whose 8 taps cover k; |d(j) - d(k)| < 1
-// for every j of the row (validated at plan creation: alpha n_rg < 1/2), so they lie in
-// j' = k - floor(d(k)) - 5 .. k - floor(d(k)) + 4 (unwrapped; j = j' mod N)
-template <int N>
-CSSAR_DEV float2 rcmc_scatter_T(const float2* p, float2 rc, int k) {
+CSSAR_DEV float2 rcmc_T_exact(const float2* row, float2 rc, int k) {
   const int jc = k - (int)floorf(rcmc_shift(rc, k, N));
   float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
   for (int c = -5; c < 5; ++c) {
     const int jp = jc + c;
     const int j = jp & (N - 1);
     const float d = rcmc_shift(rc, j, N);
-    const float fl = floorf(d);
     const int m = k - jp;
-    const int mm = m - (int)fl;
+    const int mm = m - (int)floorf(d);
     if (mm >= -3 && mm <= 4) {
-      float w;
-      if (d == fl) {
-        w = mm == 0 ? 1.0f : 0.0f;
-      } else {
-        w = __fdividef((m & 1) ? 1.0f : -1.0f, (float)m - d);
-      }
-      const float2 x = p[j];
+      const float w = sinc_md(m, d, sinpif(d) * kInvPi);
+      const float2 x = row[rsw(j)];
       acc.x = fmaf(w, x.x, acc.x);
       acc.y = fmaf(w, x.y, acc.y);
     }
@@ -110,6 +141,47 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   constexpr int LR0 = En::template lr<false>(0), LRL = En::template lr<false>(En::P - 1);
 
   float2 v[En::E];
+  static_assert(En::E == 32 && C::T * 32 == N * C::B, "RCMC chunking: 32 consecutive gates per thread");
+  // RDA: RCMC of the staged rows (s[b N + rsw(i)]) -> v in the first-pass group layout
+  auto rcmc_apply = [&](auto tr_tag, float2* sm, float2 (&vv)[En::E], int tt) {
+    constexpr bool TR = decltype(tr_tag)::value;
+    const int g = tt * 32, bb = g >> LOGN, k0 = g & (N - 1);
+    rcmc_chunk<N, TR>(sm + bb * N, a.rcmc[a.row_base + row0 + bb], k0, vv);
+    constexpr int NF = kRcmcWrapLo + kRcmcWrapHi, SL = C::B * NF, PER = (SL + C::T - 1) / C::T;
+    float2 fx[TR ? PER : 1];
+    if constexpr (TR) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int f = tt + q * C::T;
+        if (f < SL) {
+          const int fb = f / NF, sl = f % NF;
+          const int k = sl < kRcmcWrapLo ? sl : N - NF + sl;
+          fx[q] = rcmc_T_exact<N>(sm + fb * N, a.rcmc[a.row_base + row0 + fb], k);
+        }
+      }
+    }
+    __syncthreads();                    // all reads of the staged rows done
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const int k = k0 + n;
+      if (!TR || (k >= kRcmcWrapLo && k < N - kRcmcWrapHi)) sm[bb * N + rsw(k)] = vv[n];
+    }
+    if constexpr (TR) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int f = tt + q * C::T;
+        if (f < SL) {
+          const int fb = f / NF, sl = f % NF;
+          sm[fb * N + rsw(sl < kRcmcWrapLo ? sl : N - NF + sl)] = fx[q];
+        }
+      }
+    }
+    __syncthreads();
+    En::template for_groups<LR0>(vv, tt, [&](int b, int j, float2* x) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = sm[b * N + rsw(j + r * (N / R0))];
+    });
+  };
   // element j of local row rr: plain row-major, or [peer][row][w] blocks (multi-GPU)
   auto at = [&](int rr, int j) -> size_t {
     if constexpr (BLK) {
@@ -131,19 +203,13 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
       phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     });
   } else if constexpr (GBODY) {
-    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage S V
-      const int row = a.row_base + row0 + b;
-      phase_apply<R0, N / R0, true>(tab, a.coef[row].q[2], j - N / 2, x);
-      const float2 rc = a.rcmc[row];
+    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage the row
+      phase_apply<R0, N / R0, true>(tab, a.coef[a.row_base + row0 + b].q[2], j - N / 2, x);
 #pragma unroll
-      for (int r = 0; r < R0; ++r) s[b * N + j + r * (N / R0)] = rcmc_stage_T<N>(x[r], rc, j + r * (N / R0));
+      for (int r = 0; r < R0; ++r) s[b * N + rsw(j + r * (N / R0))] = x[r];
     });
     __syncthreads();
-    En::template for_groups<LR0>(v, t, [&](int b, int k, float2* x) {    // D = C^T
-      const float2 rc = a.rcmc[a.row_base + row0 + b];
-#pragma unroll
-      for (int r = 0; r < R0; ++r) x[r] = rcmc_scatter_T<N>(s + b * N, rc, k + r * (N / R0));
-    });                                 // the FFT's first exchange syncs before overwriting s
+    rcmc_apply(std::true_type{}, s, v, t);          // D = C^T; the FFT's first exchange syncs before reusing s
   }
   En::template passes_from<-1, false, 0>(s, v, t, tw);                   // range FFT
   En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
@@ -157,14 +223,10 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     __syncthreads();                    // every thread finished reading the last exchange
     En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
 #pragma unroll
-      for (int r = 0; r < R0; ++r) s[b * N + j + r * (N / R0)] = x[r];
+      for (int r = 0; r < R0; ++r) s[b * N + rsw(j + r * (N / R0))] = x[r];
     });
     __syncthreads();
-    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
-      const float2 rc = a.rcmc[a.row_base + row0 + b];
-#pragma unroll
-      for (int r = 0; r < R0; ++r) x[r] = rcmc_gather<N>(s + b * N, rc, j + r * (N / R0));
-    });
+    rcmc_apply(std::false_type{}, s, v, t);
   }
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
     if constexpr (!RDA) {

@@ -1,5 +1,5 @@
 """Per-step device times of the ITA loop on a random problem of any grid (tuning aid):
-    python tools/stage_times.py N_AZ N_RG [iters]      (GPU box; honours CSSAR_LIB)"""
+    python tools/stage_times.py N_AZ N_RG [iters [op]]      (GPU box; honours CSSAR_LIB)"""
 import json
 import os
 import sys
@@ -20,13 +20,14 @@ def main():
     mask = torch.rand((n_az, n_rg), device="cuda", generator=g) < 0.5
     Y = torch.where(mask, Y, torch.zeros_like(Y))
     mb = pack_mask(mask)
-    pl = Plan(SarParams(n_az=n_az, n_rg=n_rg))
+    op = sys.argv[4] if len(sys.argv) > 4 else "csa"
+    pl = Plan(SarParams(n_az=n_az, n_rg=n_rg), op=op)
     k = n_az * n_rg // 100
     X = torch.zeros_like(Y)
     pl.ita_iterate(Y, mb, X=X, k=k, iters=3)
     pl.ita_iterate(Y, mb, X=X, k=k, iters=iters, profile_stages=True)
     st, it = pl.stage_times()
-    print(json.dumps({"grid": [n_az, n_rg], **{kk: round(v / it, 4) for kk, v in st.items()}}))
+    print(json.dumps({"grid": [n_az, n_rg], "op": op, **{kk: round(v / it, 4) for kk, v in st.items()}}))
 
 
 if __name__ == "__main__":
