@@ -92,7 +92,12 @@ enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2 };
  * mu_i = ||dX_k||^2 / ||Theta G(dX_k)||^2, dX_k = the MF update M(Theta(Y - G X_i)) on the
  * support of X_i (eq. 27, in the normalised-IHT form of its cited source;
  * DESIGN.md R11, R20), mu_i = 1 on an empty support; the fixed-lambda rule then thresholds at
- * lambda mu_i.  Costs three more sweeps and an elementwise pass per iteration. */
+ * lambda mu_i.  Costs three more sweeps and an elementwise pass per iteration.
+ * tol > 0 (world 1 only; NEXT-4): stop after the first update with
+ * ||X_(i+1) - X_i||_F <= tol ||X_i||_F (iters stays the cap).  Needs the third workspace
+ * array (the kept X_i); per iteration one more elementwise pass (X_(i+1) vs X_i, 24 B/sample)
+ * and a host synchronisation on `stream`.  The number of updates performed is read with
+ * cssar_ita_iters_done; log entries exist only for those. */
 typedef struct {
   int32_t thr;      /* cssar_thr */
   int32_t rule;     /* cssar_rule */
@@ -101,6 +106,7 @@ typedef struct {
   double mu;
   int32_t iters;
   int32_t flags;    /* CSSAR_FLAG_* bits; 0 = graph-replayed loop */
+  double tol;       /* relative-change stopping tolerance; 0 = run `iters` updates */
 } cssar_ita_params;
 
 /* Per-iteration log (SPEC "SolverReport"): sigma_i = lambda_i mu_i, lambda_i,
@@ -137,9 +143,9 @@ int cssar_plan_destroy(cssar_plan plan);
 /* Fill id_out (host, 128 bytes) with a fresh ncclUniqueId for cssar_plan_create(world > 1). */
 int cssar_nccl_unique_id(void* id_out);
 
-/* Bytes of device workspace cssar_ita_iterate needs: world 1: two complex64 arrays of the
- * scene size (transform buffer; adaptive-step gradient) plus a candidate buffer for the exact
- * top-k select (~16.5 B/sample); world > 1:
+/* Bytes of device workspace cssar_ita_iterate needs: world 1: three complex64 arrays of the
+ * scene size (transform buffer; adaptive-step gradient; X_i of the tolerance stop) plus a
+ * candidate buffer for the exact top-k select (~24.5 B/sample); world > 1:
  * four complex64 column-slab arrays (transposes, Y, state), the column-slab mask and the
  * candidate buffer (~32.6 B per local sample). */
 int cssar_workspace_size(cssar_plan plan, size_t* bytes);
@@ -174,6 +180,9 @@ int cssar_image(cssar_plan plan, const void* Y, const uint32_t* mask_bits, void*
 int cssar_ita_iterate(cssar_plan plan, const void* Y, const uint32_t* mask_bits,
                       const cssar_ita_params* prm, void* X_inout, cssar_iter_log* log_host,
                       void* stream);
+/* Number of X updates the last cssar_ita_iterate on this plan performed (prm->iters unless
+ * the tolerance stop fired). */
+int cssar_ita_iters_done(cssar_plan plan, int32_t* iters_out);
 
 /* mask_u8 (device, rows*cols bytes, nonzero = sampled) -> bit-packed mask (rows*cols/32
  * words); cols must be a multiple of 32. */

@@ -24,6 +24,8 @@ Passages followed:
     with a fixed lambda sigma_i = lambda mu_i (soft) / the half jump point of lambda mu_i.
   * q = 0 (hard) and q = 2/3 thresholds (NEXT-4; P:L102 lists q = 0, 1/2, 2/3, 1 as the
     analytic cases): hard keeps |b| > sigma; 2/3 is the closed-form L2/3 minimiser (twothirds).
+  * tolerance stopping (NEXT-4, default tol 1e-6 at S:L387; the paper runs a
+    fixed 100 iterations): stop when ||X_(i+1) - X_i||_F <= tol ||X_i||_F.
 """
 import numpy as np
 
@@ -146,17 +148,22 @@ def adaptive_mu(op, dX, X, mask):
     return num / den if den > 0.0 and num > 0.0 else 1.0
 
 
-def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10, X0=None, log=None):
+def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10, X0=None, log=None,
+        tol=0.0, info=None):
     """Algorithm 1 with A = Theta o G. Returns X_I (complex128).
 
-    op: oracle.csa.CSAOperator; Y: echo (zero-filled where mask == 0); mask: 0/1 array.
-    mu: a positive step, or "adaptive" for the eq. 27 rule (adaptive_mu).
+    op: oracle.csa.CSAOperator (or rda.RDAOperator); Y: echo (zero-filled where mask == 0);
+    mask: 0/1 array.  mu: a positive step, or "adaptive" for the eq. 27 rule (adaptive_mu).
     log (optional list) receives per-iteration dicts: sigma, lam, mu, support, resid2, gap.
+    tol > 0 (NEXT-4; S:L371 "stop at max_iters or when ||X^(i+1) - X^(i)||_F <= tol ||X^(i)||_F"):
+    stop after the first such update.  info (optional dict) receives iters = updates performed.
     """
     Y = np.asarray(Y, dtype=np.complex128)
     m = np.asarray(mask, dtype=np.float64)
     X = np.zeros(Y.shape, np.complex128) if X0 is None else np.asarray(X0, dtype=np.complex128).copy()
-    for _ in range(iters):
+    if info is not None:
+        info["iters"] = 0
+    for it in range(iters):
         R = m * (Y - op.G(X))                      # Residue (Alg. 1 line 2)
         dX = op.M(R)                               # MF on residue (line 3); Theta already applied
         mu_i = adaptive_mu(op, dX, X, m) if mu == "adaptive" else mu
@@ -174,7 +181,12 @@ def ita(op, Y, mask, *, thr="soft", rule="k", k=None, lam=None, mu=1.0, iters=10
             if rule == "k":
                 entry["gap"] = float((a[k - 1] - a[k]) / a[k]) if a[k] > 0 else float("inf")
             log.append(entry)
+        done = tol > 0.0 and np.linalg.norm(Xn - X) <= tol * np.linalg.norm(X)
         X = Xn
+        if info is not None:
+            info["iters"] = it + 1
+        if done:
+            break
     return X
 
 

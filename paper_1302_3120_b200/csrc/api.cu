@@ -29,9 +29,10 @@ struct GraphKey {
   int thr, rule;
   long long k;
   double lambda, mu;
+  int flags;                        // the iteration body differs with CSSAR_FLAG_ADAPTIVE_MU
   bool operator==(const GraphKey& o) const {
     return Y == o.Y && mask == o.mask && X == o.X && thr == o.thr && rule == o.rule && k == o.k &&
-           lambda == o.lambda && mu == o.mu;
+           lambda == o.lambda && mu == o.mu && flags == o.flags;
   }
 };
 
@@ -56,6 +57,11 @@ struct cssar_plan_s {
   size_t ws_bytes = 0;
   float2* U = nullptr;
   float2* D = nullptr;              // adaptive step: the dense gradient dX (world 1)
+  float2* Xk = nullptr;             // tolerance stop: the kept X_i (world 1)
+  double2* d_conv = nullptr;        // tolerance stop: per-block (||X_(i+1) - X_i||^2, ||X_i||^2)
+  double2* h_conv = nullptr;        //   pinned host copy
+  int conv_blocks = 0;
+  int iters_done = 0;
   uint32_t* cand = nullptr;
   uint32_t cand_cap = 0;
   // graph cache for the iteration body
@@ -646,6 +652,8 @@ int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
     return CSSAR_ERR_BAD_MU;
   if (prm->iters < 0 || prm->iters > kLogCap) return CSSAR_ERR_INVALID_PARAMS;
   if ((prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && pl->world != 1) return CSSAR_ERR_INVALID_PARAMS;
+  if (!(prm->tol >= 0.0) || !std::isfinite(prm->tol) || (prm->tol > 0.0 && pl->world != 1))
+    return CSSAR_ERR_INVALID_PARAMS;
   return CSSAR_OK;
 }
 
@@ -661,7 +669,7 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
   if (rc != CSSAR_OK) return rc;
   if (prm.iters > 0) {
     GraphKey key{nullptr, (const void*)(uintptr_t)p0->have_mask, nullptr, prm.thr, prm.rule,
-                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu};
+                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu, 0};
     if (!*ghave || !(*gkey == key)) {
       if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
       *ghave = false;
@@ -888,7 +896,7 @@ size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
 
 // workspace layout: world 1: [U | cand]; world > 1: [Ucol | Vrow | Ycol | bcol | mcol | cand]
 size_t workspace_bytes(cssar_plan pl) {
-  if (pl->world == 1) return 2 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
+  if (pl->world == 1) return 3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
   return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + sizeof(uint32_t) * cand_capacity((long long)nl) + 256;
 }
@@ -897,7 +905,8 @@ void bind_views(cssar_plan pl, char* ws) {
   if (pl->world == 1) {
     pl->U = (float2*)ws;
     pl->D = (float2*)(ws + sizeof(float2) * (size_t)pl->n);
-    pl->cand = (uint32_t*)(ws + 2 * sizeof(float2) * (size_t)pl->n);
+    pl->Xk = (float2*)(ws + 2 * sizeof(float2) * (size_t)pl->n);
+    pl->cand = (uint32_t*)(ws + 3 * sizeof(float2) * (size_t)pl->n);
     pl->cand_cap = (uint32_t)cand_capacity(pl->n);
     return;
   }
@@ -955,6 +964,8 @@ int cssar_plan_destroy(cssar_plan pl) {
   cudaFree(pl->d_coef);
   cudaFree(pl->d_rg_tab);
   cudaFree(pl->d_rcmc);
+  cudaFree(pl->d_conv);
+  if (pl->h_conv) cudaFreeHost(pl->h_conv);
   cudaFree(pl->d_az_tab);
   cudaFree(pl->d_az_tab_r);
   cudaFree(pl->d_st);
@@ -1076,6 +1087,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   if (v != CSSAR_OK) return v;
   if (!pl->U) return CSSAR_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  pl->iters_done = prm->iters;
   if (pl->world > 1) {                          // this rank's row slabs; NCCL transposes
     Ranks R{&pl, 1};
     return ita_multi(R, &Y, &mask_bits, *prm, &X_inout, log_host, s, &pl->gexec, &pl->gkey, &pl->ghave);
@@ -1083,6 +1095,28 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   const float sigma_fixed = prm->rule == CSSAR_RULE_FIXED_LAMBDA ? (float)fixed_sigma(*prm) : 0.f;
   CUDA_TRY(launch_init_state(pl->d_st, pl->d_hist, pl->d_hist_full, prm->thr, sigma_fixed, s));
   const bool prof = (prm->flags & CSSAR_FLAG_PROFILE_STAGES) != 0;
+  const bool tol = prm->tol > 0.0;
+  if (tol) {                                   // X_0 = E(b; sigma_init) = X_inout
+    if (!pl->d_conv) {
+      pl->conv_blocks = 4 * pl->sm_count;
+      CUDA_TRY(cudaMalloc(&pl->d_conv, sizeof(double2) * pl->conv_blocks));
+      CUDA_TRY(cudaMallocHost(&pl->h_conv, sizeof(double2) * pl->conv_blocks));
+    }
+    CUDA_TRY(cudaMemcpyAsync(pl->Xk, X_inout, sizeof(float2) * (size_t)pl->n, cudaMemcpyDeviceToDevice, s));
+  }
+  // tolerance stop after update `it`: X_(it+1) = E(b_it; sigma_it) against the kept X_it
+  auto converged = [&](int it, bool& stop) -> int {
+    stop = false;
+    if (!tol) return CSSAR_OK;
+    CUDA_TRY(launch_conv_check((const float2*)X_inout, pl->Xk, pl->n, pl->d_st, prm->thr, pl->d_conv,
+                               pl->conv_blocks, s));
+    CUDA_TRY(cudaMemcpyAsync(pl->h_conv, pl->d_conv, sizeof(double2) * pl->conv_blocks, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    double d2 = 0.0, x2 = 0.0;
+    for (int i = 0; i < pl->conv_blocks; ++i) { d2 += pl->h_conv[i].x; x2 += pl->h_conv[i].y; }
+    if (std::sqrt(d2) <= prm->tol * std::sqrt(x2)) { stop = true; pl->iters_done = it + 1; }
+    return CSSAR_OK;
+  };
   if (prof) {
     for (int i = 0; i < 6; ++i) pl->stage_ms[i] = 0.0;
     pl->stage_iters = 0;
@@ -1096,10 +1130,14 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
         pl->stage_ms[i] += ms;
       }
       pl->stage_iters += 1;
+      bool stop = false;
+      rc = converged(it, stop);
+      if (rc != CSSAR_OK) return rc;
+      if (stop) break;
     }
   } else if (prm->iters > 0) {
     GraphKey key{Y, mask_bits, X_inout, prm->thr, prm->rule, prm->rule == CSSAR_RULE_KSPARSE ? prm->k : 0,
-                 prm->lambda, prm->mu};
+                 prm->lambda, prm->mu, prm->flags & CSSAR_FLAG_ADAPTIVE_MU};
     if (!pl->ghave || !(pl->gkey == key)) {
       if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
       pl->ghave = false;
@@ -1115,17 +1153,24 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       pl->gkey = key;
       pl->ghave = true;
     }
-    for (int it = 0; it < prm->iters; ++it) CUDA_TRY(cudaGraphLaunch(pl->gexec, s));
+    for (int it = 0; it < prm->iters; ++it) {
+      CUDA_TRY(cudaGraphLaunch(pl->gexec, s));
+      bool stop = false;
+      const int rc = converged(it, stop);
+      if (rc != CSSAR_OK) return rc;
+      if (stop) break;
+    }
   }
   CUDA_TRY(launch_finalize((float2*)X_inout, pl->n, prm->thr, pl->d_st, s));
   if (log_host) {
-    std::vector<IterLogDev> tmp((size_t)prm->iters);
+    const int nl = pl->iters_done;
+    std::vector<IterLogDev> tmp((size_t)nl);
     SelState st;
-    if (prm->iters > 0)
-      CUDA_TRY(cudaMemcpyAsync(tmp.data(), pl->d_log, sizeof(IterLogDev) * prm->iters, cudaMemcpyDeviceToHost, s));
+    if (nl > 0)
+      CUDA_TRY(cudaMemcpyAsync(tmp.data(), pl->d_log, sizeof(IterLogDev) * nl, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(&st, pl->d_st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    for (int i = 0; i < prm->iters; ++i) {
+    for (int i = 0; i < nl; ++i) {
       log_host[i].sigma = tmp[i].sigma;
       log_host[i].lambda = tmp[i].lam;
       log_host[i].support = tmp[i].support;
@@ -1134,6 +1179,12 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
     }
     if (st.nonfinite) return CSSAR_ERR_NONFINITE;
   }
+  return CSSAR_OK;
+}
+
+int cssar_ita_iters_done(cssar_plan pl, int32_t* iters_out) {
+  if (!pl || !iters_out) return CSSAR_ERR_BAD_PLAN;
+  *iters_out = pl->iters_done;
   return CSSAR_OK;
 }
 

@@ -139,6 +139,9 @@ cudaError_t launch_lambda_step(SelState* st, int thr, float mu, IterLogDev* log,
 // adaptive step: mu_i = mu_num/mu_den (1 if either is 0); b <- E(b; sigma_{i-1}) + mu_i D; histogram /
 // candidates / fixed-lambda support exactly as the tail kernel
 cudaError_t launch_adaptive_step(const AzArgs& a, long long n, int sm_count, cudaStream_t s);
+// tolerance stop (NEXT-4): per-block (||E(b; sigma) - Xk||^2, ||Xk||^2) into part[blocks], Xk <- E(b; sigma)
+cudaError_t launch_conv_check(const float2* b, float2* Xk, long long n, const SelState* st, int thr, double2* part,
+                              int blocks, cudaStream_t s);
 // bufs[p][i] <- sum_p bufs[p][i] for every p (single-device emulation of an all-reduce)
 cudaError_t launch_group_sum(int dtype, void* const* bufs, int world, long long count, cudaStream_t s);
 cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,

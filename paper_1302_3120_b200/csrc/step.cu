@@ -75,4 +75,44 @@ cudaError_t launch_adaptive_step(const AzArgs& a, long long n, int sm_count, cud
   return cudaGetLastError();
 }
 
+// Tolerance stop (NEXT-4): after the select of iteration i, X_(i+1) = E(b_i; sigma_i)
+// (the X the next S1 or the final pass forms) against the kept X_i.  Fixed grid, fp64 per-thread
+// sums reduced in a fixed order per block: the per-block partials are summed in block order by
+// the host, so the decision is deterministic.
+__global__ void __launch_bounds__(256) conv_check_kernel(const float4* b, float4* xk, long long n2,
+                                                         const SelState* st, int thr, double2* part) {
+  __shared__ double2 red[8];
+  const uint32_t s2 = st->sigma2_bits;
+  const float sig = st->sigma;
+  double d2 = 0.0, x2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+    const float4 bq = b[i], xq = xk[i];
+    const float2 k0 = threshold(make_float2(bq.x, bq.y), s2, sig, thr);
+    const float2 k1 = threshold(make_float2(bq.z, bq.w), s2, sig, thr);
+    const double e0 = (double)k0.x - xq.x, e1 = (double)k0.y - xq.y, e2 = (double)k1.x - xq.z, e3 = (double)k1.y - xq.w;
+    d2 += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
+    x2 += (double)xq.x * xq.x + (double)xq.y * xq.y + (double)xq.z * xq.z + (double)xq.w * xq.w;
+    xk[i] = make_float4(k0.x, k0.y, k1.x, k1.y);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d2 += __shfl_down_sync(0xffffffffu, d2, o);
+    x2 += __shfl_down_sync(0xffffffffu, x2, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = make_double2(d2, x2);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 r = red[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) { r.x += red[q].x; r.y += red[q].y; }
+    part[blockIdx.x] = r;
+  }
+}
+
+cudaError_t launch_conv_check(const float2* b, float2* Xk, long long n, const SelState* st, int thr, double2* part,
+                              int blocks, cudaStream_t s) {
+  conv_check_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(b), reinterpret_cast<float4*>(Xk), n / 2,
+                                           st, thr, part);
+  return cudaGetLastError();
+}
+
 }  // namespace cssar

@@ -29,6 +29,7 @@ SYMBOLS = [
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
     "cssar_debug_fallbacks", "cssar_stage_times", "cssar_nccl_unique_id", "cssar_group_create",
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
+    "cssar_ita_iters_done",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
@@ -52,7 +53,7 @@ OP_CODES = {"csa": 1, "rda": 2}   # cssar_op (include/cssar.h): the approximated
 class ItaParamsC(ctypes.Structure):
     _fields_ = [("thr", ctypes.c_int32), ("rule", ctypes.c_int32), ("k", ctypes.c_int64),
                 ("lam", ctypes.c_double), ("mu", ctypes.c_double), ("iters", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("tol", ctypes.c_double)]
 
 
 class IterLogC(ctypes.Structure):
@@ -93,6 +94,7 @@ def load_library(path=None):
     lib.cssar_group_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SarParamsC), I, V]
     lib.cssar_group_destroy.argtypes = [P]
     lib.cssar_group_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
+    lib.cssar_ita_iters_done.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
     lib.cssar_group_ita_iterate.argtypes = [P, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(ItaParamsC),
                                             ctypes.POINTER(V), ctypes.POINTER(IterLogC), V]
@@ -225,9 +227,10 @@ class Plan:
         return out
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
-                    log=False, profile_stages=False, stream=None):
+                    log=False, profile_stages=False, stream=None, tol=0.0):
         """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X.
-        mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU)."""
+        mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU).  tol > 0: stop after the
+        first update with ||X_(i+1) - X_i|| <= tol ||X_i|| (self.iters_done = updates performed)."""
         if X is None:
             X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
         adaptive = isinstance(mu, str)
@@ -237,14 +240,17 @@ class Plan:
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
                          int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
                          (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
-                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0))
+                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0), float(tol))
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
                                         logbuf if log else None, _stream(stream))
         _check(rc, "cssar_ita_iterate")
+        done = ctypes.c_int32()
+        _check(self.lib.cssar_ita_iters_done(self.h, ctypes.byref(done)), "cssar_ita_iters_done")
+        self.iters_done = done.value
         if log:
             entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu)
-                       for e in list(logbuf)[:iters]]
+                       for e in list(logbuf)[:self.iters_done]]
             return X, entries
         return X
 

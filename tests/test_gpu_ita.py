@@ -313,3 +313,33 @@ def test_ita_fixed_lambda_hard_and_twothirds():
                                   iters=15, log=True)
         assert rel_l2(to_host(Xg), Xo) <= TOL_ITA, thr
         assert [e["support"] for e in glog] == [e["support"] for e in olog], thr
+
+
+@pytest.mark.parametrize("name,op", [("c0", "csa"), ("c1", "csa"), ("c1", "rda")])
+def test_ita_tolerance_stop_matches_oracle(name, op):
+    """NEXT-4: the GPU stops at the same update as the oracle.  tol is placed between
+    the oracle's relative change at the stop update and every earlier one (>= 10% margins)."""
+    from oracle import rda
+    from paper_1302_3120_b200 import Plan
+    prob = problem(name)
+    cfg = prob.cfg
+    O = csa.CSAOperator(cfg.params) if op == "csa" else rda.RDAOperator(cfg.params)
+    kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu)
+    Y = prob.Y.astype(np.complex128)
+    Xs = [np.zeros(Y.shape, np.complex128)] + [ita.ita(O, Y, prob.mask, iters=j, **kw) for j in range(1, 15)]
+    r = [np.linalg.norm(Xs[j] - Xs[j - 1]) / max(np.linalg.norm(Xs[j - 1]), 1e-300) for j in range(1, 15)]
+    j = next(j for j in range(3, 15) if r[j - 1] < 0.8 * min(r[:j - 1]))
+    tol = float(np.sqrt(r[j - 1] * min(r[:j - 1])))
+    pl = Plan(cfg.params, op=op)
+    X, log = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), iters=50, tol=tol, log=True, **kw)
+    assert pl.iters_done == j and len(log) == j
+    Xg = to_host(X)
+    assert rel_l2(Xg, Xs[j]) <= 1e-3
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xs[j]).tolist())
+    # tol = 0 runs the cap; Y = 0 stops after one update with X = 0 (S:L372)
+    pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), iters=4, **kw)
+    assert pl.iters_done == 4
+    import torch
+    Z = torch.zeros_like(to_dev(prob.Y))
+    X0 = pl.ita_iterate(Z, mask_bits_dev(prob.mask), iters=30, tol=1e-6, **kw)
+    assert pl.iters_done == 1 and not torch.any(X0)

@@ -265,3 +265,37 @@ def test_twothirds_jump_phase_and_identity():
     assert abs(abs(X[0]) - sigma / 2.0) <= 1e-6 * sigma           # jumps from 0 to sigma/2
     assert abs(np.angle(X[0]) - 1.1) <= 1e-12 and X[1] == 0
     assert np.array_equal(ita.twothirds(b, 0.0), b)
+
+
+# ---- tolerance stopping (NEXT-4)
+def test_tol_stop_zero_echo_stops_after_one_update():
+    """y_s = 0 -> X* = 0 after one iteration (||X_1 - X_0|| = 0 <= tol * 0)."""
+    from inputs.configs import SarParams
+    from oracle import csa, ita
+    p = SarParams(n_az=128, n_rg=128)
+    info = {}
+    X = ita.ita(csa.CSAOperator(p), np.zeros((128, 128)), np.ones((128, 128)), k=5, iters=50, tol=1e-6, info=info)
+    assert info["iters"] == 1 and not np.any(X)
+
+
+def test_tol_stop_is_the_first_small_relative_change():
+    """The stop iteration equals the first update whose relative change, computed here from
+    separate fixed-count runs, is <= tol; the returned X is that update's."""
+    from inputs import configs, synth
+    from oracle import csa, ita
+    from tests._common import oracle_echo
+    cfg = configs.get("c0")
+    prob = synth.make_problem(cfg, oracle_echo)
+    op = csa.CSAOperator(cfg.params)
+    kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu)
+    Xs = [np.zeros(prob.Y.shape, np.complex128)] + [ita.ita(op, prob.Y, prob.mask, iters=j, **kw) for j in range(1, 13)]
+    r = [np.linalg.norm(Xs[j] - Xs[j - 1]) / max(np.linalg.norm(Xs[j - 1]), 1e-300) for j in range(1, 13)]
+    j = next(j for j in range(3, 12) if r[j - 1] < 0.8 * min(r[:j - 1]))      # a strict new minimum
+    tol = float(np.sqrt(r[j - 1] * min(r[:j - 1])))
+    info = {}
+    X = ita.ita(op, prob.Y, prob.mask, iters=40, tol=tol, info=info, **kw)
+    assert info["iters"] == j
+    assert np.array_equal(X, Xs[j])
+    info0 = {}
+    assert np.array_equal(ita.ita(op, prob.Y, prob.mask, iters=7, tol=0.0, info=info0, **kw), Xs[7])
+    assert info0["iters"] == 7
