@@ -25,10 +25,12 @@ def aperture_lines(p):
     return int(round(0.8 * p.prf ** 2 / ka))
 
 
-def exact_echo(p, targets, Na=None):
+def exact_echo(p, targets, Na=None, pulse=None):
     """Exact periodic point-target echo on the n_az x n_rg torus (complex128).
 
     targets: iterable of (i, j, sigma) in list order.
+    pulse: None for the chirp exp(+j pi Kr t^2) of eq. 1-3, or a callable t -> complex
+    (vectorised, |t| <= Tr/2) for a non-chirp transmitted pulse (NEXT-4).
     """
     n_az, n_rg = p.n_az, p.n_rg
     if Na is None:
@@ -48,8 +50,12 @@ def exact_echo(p, targets, Na=None):
         t = tau - 2.0 * R_km[:, None] / C_LIGHT
         ok = np.abs(t) <= half
         # phase in cycles, reduced mod 1 before exp (carrier term ~ 3e7 cycles)
-        cyc = 0.5 * p.Kr * t ** 2 - 2.0 * p.fc * R_km[:, None] / C_LIGHT
-        val = s_k * np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+        if pulse is None:
+            cyc = 0.5 * p.Kr * t ** 2 - 2.0 * p.fc * R_km[:, None] / C_LIGHT
+            val = s_k * np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+        else:
+            cyc = -2.0 * p.fc * R_km[:, None] / C_LIGHT * np.ones_like(t)
+            val = s_k * pulse(np.where(ok, t, 0.0)) * np.exp(2j * np.pi * (cyc - np.floor(cyc)))
         rows = ((i_k + m).astype(np.int64)[:, None] % n_az) * np.ones_like(jj)
         cols = jj % n_rg
         # m ascending then j' ascending: np.add.at accumulates in index order

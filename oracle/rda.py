@@ -18,6 +18,10 @@ Passages followed (PAPER.md = P:Lnnn):
     (R5: the grid is periodic, so taps wrap).
   * eq. 17-18, eq. 23 and Theorem 1: G = M^H with D = C^T, the literal transpose
     of the truncated kernel, conjugate filters, inverse DFTs (unitary, R4).
+  * P:L247 (NEXT-4, non-chirp pulses): "replacing P_tau* with the transmitted pulse": given
+    the recorded pulse samples s_m at tau_m = (m - (L-1)/2)/F_r, G's range filter is its
+    spectrum H(f_l) = sum_m s_m exp(-j 2 pi f_l tau_m) / sqrt(sum_m |s_m|^2) (signed bins
+    f_l, unit mean |H|^2) and M's is conj(H) (the matched filter), R38.
 Plain definition, written out: the RCMC is applied row by row as an explicit gather of the
 8 taps (C) and its transpose as the matching scatter-add (D); no blocking or fusion.
 """
@@ -28,10 +32,20 @@ from .csa import C_LIGHT, CSAGeometry, fft_az, fft_rg
 TAPS = 8  # truncated sinc kernel: 8 taps (halfwidth 4)
 
 
+def pulse_spectrum(pulse, Fr, n):
+    """H(f_l), l in fftfreq order, of pulse samples s_m at tau_m = (m - (L-1)/2)/F_r, normalised to
+    unit mean |H|^2 (a direct sum, written out)."""
+    s = np.asarray(pulse, dtype=np.complex128)
+    tau = (np.arange(s.size) - (s.size - 1) / 2.0) / Fr
+    f = np.fft.fftfreq(n, d=1.0 / Fr)
+    H = np.exp(-2j * np.pi * f[:, None] * tau[None, :]) @ s
+    return H / np.sqrt(np.sum(np.abs(s) ** 2))
+
+
 class RDAOperator:
     """M (RDA focusing, eq. 14) and G = M^H (eq. 18, Theorem 1)."""
 
-    def __init__(self, p, taps=TAPS):
+    def __init__(self, p, taps=TAPS, pulse=None):
         self.geo = CSAGeometry(p)          # axes, D(f_eta) (same definitions, SURVEY 8(c).1-2)
         self.p = p
         self.taps = taps
@@ -40,6 +54,8 @@ class RDAOperator:
         n_rg = p.n_rg
         # filters, in cycles (phase / 2 pi), then unit-modulus screens
         self.ptau = g.expc(0.5 * g.f_tau ** 2 / p.Kr)[None, :]                      # exp(+j pi f^2/K_r)
+        if pulse is not None:
+            self.ptau = np.conj(pulse_spectrum(pulse, p.Fr, n_rg))[None, :]
         lam = C_LIGHT / p.fc
         R0 = g.R0[None, :]
         f = g.f_eta[:, None]

@@ -124,3 +124,56 @@ def test_csrda_ita_recovers_targets():
     assert top == {i * p.n_rg + j for (i, j, _) in tg}
     for (i, j, s) in tg:
         assert abs(np.angle(X[i, j] / s)) < 0.02
+
+
+# ---- recorded-pulse range filter (NEXT-4: "replacing P_tau* with the transmitted pulse")
+def _nlfm(p, kappa=4e17):
+    """Non-linear FM pulse: chirp + cubic phase kappa t^3 (instantaneous frequency < F_r/2)."""
+    return lambda t: np.exp(2j * np.pi * (0.5 * p.Kr * t ** 2 + kappa * t ** 3))
+
+
+def _replica(p, fn):
+    L = int(round(p.Tr * p.Fr))
+    return fn((np.arange(L) - (L - 1) / 2.0) / p.Fr)
+
+
+def test_pulse_spectrum_closed_forms():
+    n, Fr = 64, 60e6
+    H = rda.pulse_spectrum(np.array([1.0 + 0j]), Fr, n)               # single sample: flat, unit
+    assert np.abs(H - 1.0).max() < 1e-15
+    for L in (7, 8):                                                  # rectangle: Dirichlet kernel
+        H = rda.pulse_spectrum(np.ones(L), Fr, n)
+        l = np.fft.fftfreq(n, d=1.0 / n)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            D = np.where(l == 0, L, np.sin(np.pi * l * L / n) / np.sin(np.pi * l / n))
+        assert np.abs(H - D / np.sqrt(L)).max() < 1e-12
+
+
+def test_pulse_pair_theorem1():
+    p = SarParams(n_az=64, n_rg=128)
+    op = rda.RDAOperator(p, pulse=_replica(p, _nlfm(p)))
+    X, Y = _rand(op.shape, 21), _rand(op.shape, 22)
+    assert abs(np.vdot(op.G(X), Y) - np.vdot(X, op.M(Y))) / abs(np.vdot(X, op.M(Y))) < 1e-12
+
+
+def test_nonchirp_echo_focuses_with_the_replica_only():
+    """NLFM echo (eq. 1-3 with the cubic-phase pulse): the replica-filter pair focuses each
+    target to its pixel with phase arg(sigma) - pi/4 (the matched filter cancels the range
+    spectrum's phase; the azimuth stationary-phase -pi/4 that the chirp P_tau's missing +pi/4
+    cancels for the chirp pair stays), peak 333.7 sqrt(F_r/B_r) |sigma| (|H|^2 = F_r/B_r in
+    band), the theoretical IRW and the sinc PSLR; the chirp filter misfocuses the same echo."""
+    p = SarParams(n_az=128, n_rg=256)
+    tg = [(64, 128, np.exp(0.4j)), (20, 40, 1.0)]
+    Y = echo.exact_echo(p, tg, pulse=_nlfm(p))
+    img = rda.RDAOperator(p, pulse=_replica(p, _nlfm(p))).M(Y)
+    bad = rda.RDAOperator(p).M(Y)
+    th = _theory(p)
+    for (i, j, s) in tg:
+        win = metrics.chip(np.abs(img), i, j, size=8)
+        assert np.unravel_index(np.argmax(win), win.shape) == (4, 4)
+        assert abs(np.angle(img[i, j] / s * np.exp(0.25j * np.pi))) < GOLD["phase_tol_rad"]
+        assert abs(abs(img[i, j]) / (th["peak"] * np.sqrt(p.Fr / (p.Kr * p.Tr))) - 1) < GOLD["peak_rel_tol"]
+        q = metrics.point_target_quality(img, i, j, p)
+        assert abs(q["irw_rg"] / th["irw_rg"] - 1) < GOLD["irw_rel_tol"], q
+        assert abs(q["pslr_rg"] - GOLD["pslr_sinc_db"]) < GOLD["pslr_tol_db"], q
+        assert abs(bad[i, j]) < 0.5 * abs(img[i, j])
