@@ -180,6 +180,17 @@ int cssar_image(cssar_plan plan, const void* Y, const uint32_t* mask_bits, void*
 int cssar_ita_iterate(cssar_plan plan, const void* Y, const uint32_t* mask_bits,
                       const cssar_ita_params* prm, void* X_inout, cssar_iter_log* log_host,
                       void* stream);
+/* RDA plans (CSSAR_OP_RDA) only — non-chirp pulses (NEXT-4: "replacing P_tau* with
+ * the transmitted pulse, which is always recorded"): pulse_host = len complex64 samples
+ * (interleaved re, im; host) of the recorded transmitted pulse at range times
+ * (m - (len-1)/2)/F_r, 1 <= len <= n_rg.  G's range filter becomes its spectrum
+ * H(f_l) = sum_m s_m exp(-j 2 pi f_l tau_m) / sqrt(sum_m |s_m|^2) (signed bins, unit mean |H|^2)
+ * and M's the matched filter conj(H), in place of the chirp P_tau.  len = 0 restores the chirp.
+ * Synchronous (host DFT in long double, O(n_rg len)); drops the cached iteration graph.
+ * Errors: CSSAR_ERR_BAD_PLAN (NULL or a CSA plan), CSSAR_ERR_INVALID_PARAMS (len out of range,
+ * zero-energy or non-finite pulse). */
+int cssar_plan_set_pulse(cssar_plan plan, const void* pulse_host, int64_t len);
+
 /* Number of X updates the last cssar_ita_iterate on this plan performed (prm->iters unless
  * the tolerance stop fired). */
 int cssar_ita_iters_done(cssar_plan plan, int32_t* iters_out);

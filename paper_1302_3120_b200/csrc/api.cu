@@ -46,6 +46,7 @@ struct cssar_plan_s {
   RowCoef* d_coef = nullptr;
   float2* d_rg_tab = nullptr;     // phase exp table + range-engine twiddles
   float2* d_rcmc = nullptr;       // RDA plans: per-row RCMC migration (alpha, s0); CSA: nullptr
+  float2* d_hrange = nullptr;     // RDA plans with a recorded pulse: G's range filter H (n_rg)
   float2* d_az_tab = nullptr;     // azimuth-engine twiddles (head / tail / operator kernels)
   float2* d_az_tab_r = nullptr;   // azimuth-engine twiddles (residual kernel)
   SelState* d_st = nullptr;
@@ -286,6 +287,7 @@ int enqueue_forward(cssar_plan pl, const void* X, const uint32_t* mask, void* Yo
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_PLAIN, a.n_rg, a, s));
   RgArgs r{(float2*)Yout, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
+  r.hrange = pl->d_hrange;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Yout;
   a.mask = mask;
@@ -306,6 +308,7 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
   CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_MASK, a.n_rg, a, s));
   RgArgs r{(float2*)Xout, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
+  r.hrange = pl->d_hrange;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, false, (int)pl->p.n_az, r, s));
   a.in = (const float2*)Xout;
   a.mask = nullptr;
@@ -335,6 +338,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   float2* b = (float2*)X;
   RgArgs r{pl->U, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
+  r.hrange = pl->d_hrange;
   MARK(0);
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
   a.in = b;
@@ -466,6 +470,7 @@ AzArgs az_col_args(cssar_plan pl, const cssar_ita_params& prm) {
 RgArgs rg_row_args(cssar_plan pl) {
   RgArgs r{pl->Vrow, pl->d_coef, (int)(pl->rank * pl->nrow), pl->d_rg_tab, 0, 0};
   r.rcmc = pl->d_rcmc;
+  r.hrange = pl->d_hrange;
   r.log_w = ilog2_exact(pl->ncol);
   r.blk = pl->nrow * pl->ncol;
   return r;
@@ -964,6 +969,7 @@ int cssar_plan_destroy(cssar_plan pl) {
   cudaFree(pl->d_coef);
   cudaFree(pl->d_rg_tab);
   cudaFree(pl->d_rcmc);
+  cudaFree(pl->d_hrange);
   cudaFree(pl->d_conv);
   if (pl->h_conv) cudaFreeHost(pl->h_conv);
   cudaFree(pl->d_az_tab);
@@ -1182,6 +1188,44 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   return CSSAR_OK;
 }
 
+int cssar_plan_set_pulse(cssar_plan pl, const void* pulse_host, int64_t len) {
+  if (!pl || pl->p.op != CSSAR_OP_RDA) return CSSAR_ERR_BAD_PLAN;
+  const long long N = pl->p.n_rg;
+  if (len < 0 || len > N || (len > 0 && !pulse_host)) return CSSAR_ERR_INVALID_PARAMS;
+  if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
+  pl->ghave = false;
+  if (len == 0) {
+    CUDA_TRY(cudaFree(pl->d_hrange));
+    pl->d_hrange = nullptr;
+    return CSSAR_OK;
+  }
+  // H(f_l) = sum_m s_m exp(-j 2 pi l' (m - (L-1)/2) / N) / sqrt(sum |s_m|^2), l' the signed bin:
+  // the phase l' (2m - L + 1) / (2N) cycles is reduced exactly in integers before the sincos
+  const float* sp = static_cast<const float*>(pulse_host);
+  long double e = 0.0L;
+  for (long long m = 0; m < len; ++m) e += (long double)sp[2 * m] * sp[2 * m] + (long double)sp[2 * m + 1] * sp[2 * m + 1];
+  if (!(e > 0.0L) || !std::isfinite((double)e)) return CSSAR_ERR_INVALID_PARAMS;
+  const long double nrm = 1.0L / sqrtl(e);
+  const long long twoN = 2 * N;
+  std::vector<float2> H((size_t)N);
+  for (long long l = 0; l < N; ++l) {
+    const long long ls = l < N / 2 ? l : l - N;
+    long double re = 0.0L, im = 0.0L;
+    for (long long m = 0; m < len; ++m) {
+      long long k = (ls * (2 * m - len + 1)) % twoN;
+      if (k < 0) k += twoN;
+      const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)k / (long double)twoN;
+      const long double c = cosl(ang), sn = sinl(ang);
+      re += sp[2 * m] * c - sp[2 * m + 1] * sn;
+      im += sp[2 * m] * sn + sp[2 * m + 1] * c;
+    }
+    H[(size_t)l] = float2{(float)(re * nrm), (float)(im * nrm)};
+  }
+  if (!pl->d_hrange) CUDA_TRY(cudaMalloc(&pl->d_hrange, sizeof(float2) * (size_t)N));
+  CUDA_TRY(cudaMemcpy(pl->d_hrange, H.data(), sizeof(float2) * (size_t)N, cudaMemcpyHostToDevice));
+  return CSSAR_OK;
+}
+
 int cssar_ita_iters_done(cssar_plan pl, int32_t* iters_out) {
   if (!pl || !iters_out) return CSSAR_ERR_BAD_PLAN;
   *iters_out = pl->iters_done;
@@ -1200,6 +1244,7 @@ int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
   RgArgs r{(float2*)U, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
+  r.hrange = pl->d_hrange;
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, gbody != 0, (int)pl->p.n_az, r, (cudaStream_t)stream));
   return CSSAR_OK;
 }

@@ -103,6 +103,9 @@ struct RgArgs {
   // RDA operator pair (NEXT-2; cssar_sar_params::op = CSSAR_OP_RDA): per global Doppler row
   // (alpha, s0) of the RCMC migration d(j) = s0 + alpha (j - n_rg/2) range cells; nullptr = CSA
   const float2* rcmc;
+  // RDA with a recorded pulse (NEXT-4): G's range filter H(f_l) in fftfreq order (M uses
+  // conj H) instead of the chirp P_tau quadratic q[1]; nullptr = chirp
+  const float2* hrange;
 };
 
 enum AzMode : int {

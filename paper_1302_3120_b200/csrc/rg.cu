@@ -212,12 +212,29 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     rcmc_apply(std::true_type{}, s, v, t);          // D = C^T; the FFT's first exchange syncs before reusing s
   }
   En::template passes_from<-1, false, 0>(s, v, t, tw);                   // range FFT
-  En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
-    const Quad q = a.coef[a.row_base + row0 + b].q[1];
-    // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
-    phase_apply<RL / 2, N / RL, GBODY>(tab, q, j, x);
-    phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
-  });
+  auto mid_quad = [&]() {
+    En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
+      const Quad q = a.coef[a.row_base + row0 + b].q[1];
+      // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
+      phase_apply<RL / 2, N / RL, GBODY>(tab, q, j, x);
+      phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
+    });
+  };
+  if constexpr (RDA) {
+    if (a.hrange) {                     // recorded-pulse filter: H (G body) / conj H (M body)
+      En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const float2 h = __ldg(a.hrange + j + r * (N / RL));
+          x[r] = GBODY ? cmul(x[r], h) : cmulc(x[r], h);
+        }
+      });
+    } else {
+      mid_quad();
+    }
+  } else {
+    mid_quad();
+  }
   En::template passes_from<+1, true, 0>(s, v, t, tw);                    // range IFFT
   if constexpr (RDA && !GBODY) {                                          // C on the whole row
     __syncthreads();                    // every thread finished reading the last exchange

@@ -29,7 +29,7 @@ SYMBOLS = [
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
     "cssar_debug_fallbacks", "cssar_stage_times", "cssar_nccl_unique_id", "cssar_group_create",
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
-    "cssar_ita_iters_done",
+    "cssar_ita_iters_done", "cssar_plan_set_pulse",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
@@ -95,6 +95,7 @@ def load_library(path=None):
     lib.cssar_group_destroy.argtypes = [P]
     lib.cssar_group_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
     lib.cssar_ita_iters_done.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.cssar_plan_set_pulse.argtypes = [P, V, I64]
     lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
     lib.cssar_group_ita_iterate.argtypes = [P, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(ItaParamsC),
                                             ctypes.POINTER(V), ctypes.POINTER(IterLogC), V]
@@ -253,6 +254,17 @@ class Plan:
                        for e in list(logbuf)[:self.iters_done]]
             return X, entries
         return X
+
+    def set_pulse(self, pulse=None):
+        """RDA plans: recorded transmitted pulse (complex samples at (m - (L-1)/2)/F_r) as the range
+        filter; None restores the chirp P_tau."""
+        if pulse is None:
+            _check(self.lib.cssar_plan_set_pulse(self.h, None, 0), "cssar_plan_set_pulse")
+            return
+        import numpy as np
+        buf = np.ascontiguousarray(np.asarray(pulse, dtype=np.complex64))
+        _check(self.lib.cssar_plan_set_pulse(self.h, buf.ctypes.data_as(ctypes.c_void_p), buf.size),
+               "cssar_plan_set_pulse")
 
     def stage_times(self):
         """Per-step device milliseconds (summed) of the last profile_stages run, and its iterations."""

@@ -47,6 +47,9 @@ def test_null_plan_is_rejected_without_gpu():
     assert lib.cssar_plan_destroy(None) == -10
     n = ctypes.c_size_t()
     assert lib.cssar_workspace_size(None, ctypes.byref(n)) == -10
+    assert lib.cssar_plan_set_pulse(None, None, 0) == -10
+    it = ctypes.c_int32()
+    assert lib.cssar_ita_iters_done(None, ctypes.byref(it)) == -10
 
 
 def test_product_path_does_not_use_the_oracle():

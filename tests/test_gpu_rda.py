@@ -129,3 +129,60 @@ def test_rda_group_is_bitwise_single_gpu(world):
     Xg = np.concatenate([to_host(x) for x in Xg], axis=0)
     assert np.array_equal(Xg.view(np.uint32), to_host(Xs).view(np.uint32))
     assert [e["sigma"] for e in lg] == [e["sigma"] for e in ls]
+
+
+# ---- recorded-pulse range filter (NEXT-4)
+def _nlfm_replica(p, kappa=4e17):
+    L = int(round(p.Tr * p.Fr))
+    t = (np.arange(L) - (L - 1) / 2.0) / p.Fr
+    return np.exp(2j * np.pi * (0.5 * p.Kr * t ** 2 + kappa * t ** 3))
+
+
+@pytest.mark.parametrize("n_rg", [256, 8192])
+@pytest.mark.parametrize("gbody", [1, 0])
+def test_pulse_range_sweep_matches_oracle(n_rg, gbody):
+    p = SarParams(n_az=128, n_rg=n_rg)
+    s = _nlfm_replica(p)
+    U = rand_c((128, n_rg), 500 + n_rg + gbody)
+    ref = rda.RDAOperator(p, pulse=s).range_segment(U.astype(np.complex128), conj=bool(gbody))
+    pl = _plan(p, workspace=False)
+    pl.set_pulse(s)
+    d = to_dev(U)
+    pl.debug_range_sweep(d, gbody)
+    assert rel_l2(to_host(d) / n_rg, ref) <= 5e-6
+
+
+def test_pulse_operators_ita_and_reset():
+    from inputs.configs import SarParams as SP
+    from oracle import echo
+    p = SP(n_az=256, n_rg=512)
+    s = _nlfm_replica(p)
+    kap = 4e17
+    tg = [(128, 256, np.exp(0.4j)), (30, 60, 1.0), (200, 400, 0.7j), (90, 480, -1.0)]
+    Y0 = echo.exact_echo(p, tg, pulse=lambda t: np.exp(2j * np.pi * (0.5 * p.Kr * t ** 2 + kap * t ** 3)))
+    mask = (np.random.default_rng(31).random(Y0.shape) < 0.3).astype(np.uint8)
+    Y = (Y0 * mask).astype(np.complex64)
+    op = rda.RDAOperator(p, pulse=s)
+    pl = _plan(p)
+    ref_plain = to_host(pl.forward(to_dev(rand_c(Y.shape, 1)), None))
+    pl.set_pulse(s)
+    X = rand_c(Y.shape, 2)
+    mb = mask_bits_dev(mask)
+    assert rel_l2(to_host(pl.forward(to_dev(X), mb)), op.A(X.astype(np.complex128), mask)) <= 1e-5
+    assert rel_l2(to_host(pl.adjoint(to_dev(X), mb)), op.AH(X.astype(np.complex128), mask)) <= 1e-5
+    Xo = ita.ita(op, Y.astype(np.complex128), mask, thr="soft", rule="k", k=8, mu=1.0, iters=25)
+    Xg, _ = pl.ita_iterate(to_dev(Y), mb, thr="soft", rule="k", k=8, mu=1.0, iters=25, log=True)
+    Xg = to_host(Xg)
+    assert rel_l2(Xg, Xo) <= 1e-3
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
+    assert {i * p.n_rg + j for (i, j, _) in tg} <= set(np.argsort(-np.abs(Xg).ravel())[:8].tolist())
+    pl.set_pulse(None)                                   # back to the chirp P_tau, bitwise
+    assert np.array_equal(to_host(pl.forward(to_dev(rand_c(Y.shape, 1)), None)), ref_plain)
+
+
+def test_pulse_rejected_on_csa_plans():
+    from paper_1302_3120_b200 import Plan, CssarError
+    pl = Plan(SarParams(n_az=128, n_rg=128), workspace=False)
+    with pytest.raises(CssarError) as e:
+        pl.set_pulse(np.ones(4, np.complex64))
+    assert e.value.code == -10
