@@ -37,7 +37,7 @@ class Config:
     scene: str                   # scene recipe id (inputs.synth)
     scene_args: dict = field(default_factory=dict)
     echo: str = "exact"          # "exact" (periodic point-target echo) | "inverse_csa" (G(X_true))
-    mask: str = "bernoulli"      # "bernoulli" per sample | "lines" per azimuth line
+    mask: str = "bernoulli"      # "bernoulli" per sample | "lines" per azimuth line | "separable" (1:5)
     rate: float = 0.5            # sampling rate
     snr_db: float = 30.0
     thr: str = "soft"            # "soft" (q=1, eq. 9) | "half" (q=1/2)
@@ -73,6 +73,12 @@ CONFIGS = {
                  scene_args=dict(frac=0.005),
                  echo="inverse_csa", mask="bernoulli", rate=0.5, snr_db=20.0, thr="soft", rule="k",
                  k=2684355, iters=50, seed=13023120 + 4),
+    # NEXT-3: the paper's reconstruction-ability experiment: 9 targets 6 samples
+    # apart, 20 dB noise, k = 18, separable s_a : s_r = 1 : 5 sampling, 100
+    # iterations; 256 x 256 stands in for the 180 x 180 scene (power-of-two grid, R33)
+    "ra": Config("ra", _p(256, 256), scene="grid9", scene_args=dict(spacing=6),
+                 echo="exact", mask="separable", rate=0.1, snr_db=20.0, thr="soft", rule="k",
+                 k=18, iters=100, seed=13023120 + 10),
 }
 
 

@@ -128,6 +128,18 @@ def make_scene(cfg: Config) -> Scene:
             order = np.argsort(idx)
             return Scene(idx[order], val[order], (n_az, n_rg), targets)
         return Scene(base, val, (n_az, n_rg), [])
+    if cfg.scene == "grid9":
+        # P:L501 / P:L390: 9 targets "located at the center with intervals of 6 samples", unit
+        # amplitude, uniform random phase (a 3 x 3 grid, R39)
+        sp = a.get("spacing", 6)
+        ph = r_amp.uniform(0.0, 2 * np.pi, size=9)
+        ci, cj = n_az // 2, n_rg // 2
+        for q in range(9):
+            targets.append((ci + (q // 3 - 1) * sp, cj + (q % 3 - 1) * sp, complex(np.exp(1j * ph[q]))))
+        idx = np.array([i * n_rg + j for i, j, _ in targets], dtype=np.int64)
+        val = np.array([v for _, _, v in targets])
+        order = np.argsort(idx)
+        return Scene(idx[order], val[order], (n_az, n_rg), targets)
     raise ValueError(f"unknown scene recipe {cfg.scene}")
 
 
@@ -140,6 +152,14 @@ def make_mask(cfg: Config) -> np.ndarray:
         return np.repeat(keep[:, None], p.n_rg, axis=1)
     if cfg.mask == "full":
         return np.ones((p.n_az, p.n_rg), dtype=bool)
+    if cfg.mask == "separable":
+        # random azimuth lines at rate s_a, random range samples per kept line at rate
+        # s_r, s_a : s_r = 1 : 5, s_a s_r = rate (so rate <= 1/5)
+        if not 0.0 < cfg.rate <= 0.2:
+            raise ValueError("separable 1:5 sampling needs 0 < rate <= 0.2")
+        s_a, s_r = np.sqrt(cfg.rate / 5.0), np.sqrt(5.0 * cfg.rate)
+        rows = r_mask.random(p.n_az) < s_a
+        return rows[:, None] & (r_mask.random((p.n_az, p.n_rg)) < s_r)
     M = np.empty((p.n_az, p.n_rg), dtype=bool)
     for r0 in range(0, p.n_az, _CHUNK_ROWS):
         r1 = min(p.n_az, r0 + _CHUNK_ROWS)
