@@ -31,6 +31,8 @@ BYTES_PER_SAMPLE = {  # algorithmic HBM bytes per sample per launch (DESIGN.md "
     "S6_select": 0.0,
 }
 ITER_BYTES_PER_SAMPLE = 96.125     # k-rule, SURVEY.md 8(a)
+# BASELINE.json's metric; `value` is its complex samples*iter/s part (it_per_s rides along)
+METRIC = "ITA iterations/sec and complex samples\u00b7iter/s vs HBM roofline, 1/2/4/8 B200"
 
 
 def parse():
@@ -168,10 +170,11 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     sample = f"{args.config} recipe on a {n_az}x{n_rg} grid (k = {cfg.k}), one ITA iteration per step"
     line = {
-        "impl": "reference", "metric": "ITA complex samples*iterations/s", "value": value, "unit": "samples*it/s",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples*it/s",
+        "n_gpus": args.gpus, "device": "host cpu (the oracle)", "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (bounded sample {n_az}x{n_rg})", "iters_per_step": 1},
+        "config": {"workload": f"{args.config}: bounded sample of the recipe on {n_az}x{n_rg} (k = {cfg.k})",
+                   "n_az": n_az, "n_rg": n_rg, "k": cfg.k, "iters_per_step": 1},
         "cpu_baseline": {"value": value, "unit": "samples*it/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "samples*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -261,7 +264,7 @@ def main():
 
     iter_ach = ITER_BYTES_PER_SAMPLE * n * it_s / 1e9
     line = {
-        "metric": "ITA complex samples*iterations/s (HBM roofline fraction alongside)",
+        "metric": METRIC,
         "value": value, "unit": "samples*it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "it_per_s": it_s, "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong",
