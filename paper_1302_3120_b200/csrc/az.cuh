@@ -472,6 +472,15 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   // BS (TAIL, one stage): b_{i-1} of the output rows arrives by TMA into the stage buffer once the
   // local transform has read it; the next panel's stage load is issued after the epilogue
   constexpr bool BS = MODE == AZ_TAIL && NS == 1;
+  // PP (RESID/GRAD with XS, TAIL with BS): the stage and the receive buffer swap roles every
+  // panel, so the next panel's TMA load goes into the receive buffer as soon as it is consumed
+  // (mid-panel) instead of into the stage after the panel's last use of it; the cluster arrive
+  // that lets peers push into a CTA's receive buffer moves to the end of the panel
+#if defined(CSSAR_AZ_NO_PP)
+  constexpr bool PP = false;
+#else
+  constexpr bool PP = (RES && Cf::XS) || BS;
+#endif
   constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK ||
                       MODE == AZ_NORM;
   static_assert(C > 1, "cluster kernel");
@@ -487,8 +496,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   // would lose the shared address space and turn every SMEM access into a generic one)
   char* base = reinterpret_cast<char*>(smem4) + ((1024u - (smem_u32(smem4) & 1023u)) & 1023u);
   float2* stages = reinterpret_cast<float2*>(base);
-  float2* rbuf = stages + (size_t)NS * M * W;                      // pushed partial transforms [c][k][w]
-  float2* const xbuf0 = rbuf + (size_t)M * W;                       // RESID scatter target (!XS)
+  float2* const rbuf0 = stages + (size_t)NS * M * W;               // pushed partial transforms [c][k][w]
+  float2* const xbuf0 = rbuf0 + (size_t)M * W;                      // RESID scatter target (!XS)
   float2* tw = reinterpret_cast<float2*>(base + Cf::CL_TW_OFF);
   float2* ctw = reinterpret_cast<float2*>(base + Cf::CL_CTW_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cf::CL_BAR_OFF);
@@ -541,11 +550,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   }
   float racc = 0.f;
 
-  auto issue = [&](int panel, int sidx) {       // one thread: arm the stage barrier, M/BM boxes
+  auto issue = [&](int panel, int sidx, float2* dst) {   // one thread: arm the stage barrier, M/BM boxes
     const uint32_t bar = smem_u32(&full[sidx]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(Cf::STAGE_BYTES)
                  : "memory");
-    float2* dst = stages + (size_t)sidx * M * W;
 #pragma unroll
     for (int bx = 0; bx < M / BM; ++bx) {
       asm volatile(
@@ -565,7 +573,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     for (int i = 0; i < NS; ++i)
-      if (cid + i * ncl < npan) issue(cid + i * ncl, i);
+      if (cid + i * ncl < npan) issue(cid + i * ncl, i, stages + (size_t)i * M * W);
   }
   __syncthreads();
   // barrier initialisation visible cluster-wide before any remote st.async (once per kernel)
@@ -575,6 +583,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   for (int panel = cid; panel < npan; panel += ncl, ++it) {
     const int sidx = it % NS;
     float2* s = stages + (size_t)sidx * M * W;
+    float2* rbuf = rbuf0;
+    if constexpr (PP) {
+      if (it & 1) { s = rbuf0; rbuf = stages; }
+    }
     const int col0 = panel * W;
     const int next = panel + NS * ncl;
     // epilogue / residual inputs of output rows k + M q (in flight during the FFT)
@@ -656,7 +668,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       __syncthreads();                             // stage fully read: refill it NS panels ahead
       if (t == 0 && next < npan) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(next, sidx);
+        issue(next, sidx, s);
       }
     }
     // push local output k of every column to its owner rank k / (M/C): rbuf[(rank M/C + k%(M/C)) W + w]
@@ -705,7 +717,14 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       }
     }
     consume(z, misc + 40);
-    cl_arrive();                                   // rbuf (and, RESID, last panel's xbuf) consumed
+    if constexpr (!(PP && BS)) cl_arrive();        // rbuf (and, RESID, last panel's xbuf) consumed
+    if constexpr (PP) {
+      __syncthreads();                             // every thread done with the receive buffer:
+      if (t == 0 && next < npan) {                 // it becomes the next panel's stage
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(next, sidx, rbuf);
+      }
+    }
     if constexpr (RES) {
 #pragma unroll
       mbar_wait_cta(yfull, (uint32_t)(it & 1));
@@ -721,7 +740,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         cluster_twiddles<C, -1, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);     // w_N^{-q k}
       }
       cl_wait();                                   // peers are done with their scatter buffers
-      cl_arrive();                                 // (pairs with the next panel's push wait)
+      if constexpr (!PP) cl_arrive();              // (pairs with the next panel's push wait)
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
         const int pr = p * T + t;
@@ -740,11 +759,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       };
       En::template run_from_smem<-1>(xbuf, st, tw);
-      if constexpr (Cf::XS) {
+      if constexpr (PP) {
+        cl_arrive();                               // stage free: peers may push into it next panel
+      } else if constexpr (Cf::XS) {
         __syncthreads();                           // last transform done with the stage
         if (t == 0 && next < npan) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          issue(next, sidx);
+          issue(next, sidx, s);
         }
       }
     } else if constexpr (VEC) {
@@ -791,11 +812,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         if (t == 0) tc.scount[0] = 0u;
       }
     }
-    if constexpr (BS) {
+    if constexpr (PP && BS) {
+      cl_arrive();                                 // stage (b) read: peers may push into it next panel
+    } else if constexpr (BS) {
       __syncthreads();                             // every b of the panel read from the stage
       if (t == 0 && next < npan) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(next, sidx);
+        issue(next, sidx, s);
       }
     }
   }
