@@ -42,6 +42,20 @@ struct AzCfg<12, true> {
   static constexpr bool XS = true;
 };
 #endif
+#if defined(CSSAR_AZ15_C)
+template <>
+struct AzCfg<15, false> {
+  static constexpr int C = CSSAR_AZ15_C, W = CSSAR_AZ15_W, E = CSSAR_AZ15_E, NS = 1;
+  static constexpr bool XS = false;
+};
+#endif
+#if defined(CSSAR_AZ15R_C)
+template <>
+struct AzCfg<15, true> {
+  static constexpr int C = CSSAR_AZ15R_C, W = CSSAR_AZ15R_W, E = CSSAR_AZ15R_E, NS = 1;
+  static constexpr bool XS = true;
+};
+#endif
 #if defined(CSSAR_AZ13R_C)
 template <>
 struct AzCfg<13, true> {
