@@ -343,3 +343,21 @@ def test_ita_tolerance_stop_matches_oracle(name, op):
     Z = torch.zeros_like(to_dev(prob.Y))
     X0 = pl.ita_iterate(Z, mask_bits_dev(prob.mask), iters=30, tol=1e-6, **kw)
     assert pl.iters_done == 1 and not torch.any(X0)
+
+
+@pytest.mark.parametrize("n_az,n_rg,op", [(4096, 256, "csa"), (16384, 128, "csa"), (16384, 128, "rda"),
+                                          (8192, 512, "rda")])
+def test_ita_tall_grids_every_cluster_shape(n_az, n_rg, op):
+    """Azimuth lengths whose sweeps use 4- and 16-CTA clusters (n_az 4096, 16384) and the
+    c3 shape's (8192) through the residual and tail kernels (stage / receive ping-pong),
+    4 iterations of the c2 recipe vs the oracle."""
+    from oracle import rda
+    from paper_1302_3120_b200 import Plan
+    prob = problem("c2", n_az, n_rg)
+    cfg = prob.cfg
+    O = csa.CSAOperator(cfg.params) if op == "csa" else rda.RDAOperator(cfg.params)
+    Xo = ita.ita(O, prob.Y.astype(np.complex128), prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu,
+                 iters=4)
+    Xg = to_host(Plan(cfg.params, op=op).ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr,
+                                                       rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=4))
+    assert rel_l2(Xg, Xo) <= TOL_ITA
