@@ -12,8 +12,9 @@ than L2 (126 MB), so no L2 flush is needed between steps.
 
 Prints ONE JSON line (rank 0).  value = complex samples * iterations / s of the scene.
 N > 1 (torchrun): the SAME c3 scene slab-partitioned over the ranks by azimuth lines
-(NCCL all-to-all transposes between range and azimuth sweeps, reduced exact
-select) -> "scaling": "strong"; the time is the max over ranks.
+(transposes fused into the sweeps as peer-memory stores (NCCL all-to-all if the
+peers cannot be mapped), the sparse-X' first sweep, reduced exact select) -> "scaling":
+"strong"; the time is the max over ranks.
 """
 import argparse
 import json
@@ -207,6 +208,8 @@ def main():
     X = torch.zeros_like(Y)
     kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
     if world > 1:
+        kw["sparse"] = True           # sparse-X' schedule where it applies (CSSAR_FLAG_SPARSE_X)
+    if world > 1:
         # strong scaling: ONE scene slab-partitioned by azimuth lines; NCCL
         # all-to-all transposes inside libcssar, communicator from a broadcast unique id
         from paper_1302_3120_b200 import nccl_unique_id, slab_rows
@@ -273,13 +276,15 @@ def main():
                                f"{cfg.rate}, SNR {cfg.snr_db} dB, {cfg.thr} threshold, k = {cfg.k}, mu = {cfg.mu}",
                    "n_az": p.n_az, "n_rg": p.n_rg, "k": cfg.k, "l2": "inputs larger than L2 (512 MiB arrays)",
                    "parallelism": "single" if world == 1 else
-                   f"slab{world} (azimuth-line row slabs, NCCL all-to-all transposes, reduced select)"},
+                   f"slab{world} (azimuth-line row slabs; transposes fused into the sweeps as peer-memory "
+                   f"stores, or NCCL all-to-all; sparse-X' S1; reduced select)"},
         "roofline": roof,
         "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak * world, "unit": "GB/s",
                                "frac": iter_ach / (peak * world), "bytes_per_sample": ITER_BYTES_PER_SAMPLE,
                                "note": "aggregate over ranks; excludes NVLink transpose bytes" if world > 1 else None},
         "stages_ms": stages,
-        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if world == 1 else (12 if cfg.rule == "k" else 6)) + 2,
+        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if world == 1 else
+                                       ((14 if world <= 8 else 12) if cfg.rule == "k" else 6)) + 2,
         "select_fallbacks": plan.debug_fallbacks(),
         "clocks": clocks,
     }

@@ -84,7 +84,7 @@ typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 
 /* flags: CSSAR_FLAG_PROFILE_STAGES launches the iteration body directly (no graph) with CUDA
  * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
  * accumulates per-step device time (read with cssar_stage_times). */
-enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2 };
+enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPARSE_X = 4 };
 
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
  * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule.
@@ -97,7 +97,15 @@ enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2 };
  * ||X_(i+1) - X_i||_F <= tol ||X_i||_F (iters stays the cap).  Needs the third workspace
  * array (the kept X_i); per iteration one more elementwise pass (X_(i+1) vs X_i, 24 B/sample)
  * and a host synchronisation on `stream`.  The number of updates performed is read with
- * cssar_ita_iters_done; log entries exist only for those. */
+ * cssar_ita_iters_done; log entries exist only for those.
+ * CSSAR_FLAG_SPARSE_X (world > 1; a request): the sparse-X' schedule where
+ * it applies — k-rule, peer-memory transposes, k <= n_az n_rg / (8 world),
+ * n_az / world >= 128; otherwise the dense schedule runs.  From iteration 1 on, S1 and its
+ * transpose are replaced by a compacted X = E(b) (<= k entries of 16 B) that every rank
+ * pulls from every other rank's workspace, folds into n_az/world Doppler bins (cyclic
+ * distribution) and transforms locally.  Same results up to floating-point order (not
+ * bitwise equal to world 1: another FFT factorisation and atomically summed folds).
+ * world == 1: CSSAR_ERR_INVALID_PARAMS. */
 typedef struct {
   int32_t thr;      /* cssar_thr */
   int32_t rule;     /* cssar_rule */

@@ -92,6 +92,13 @@ struct cssar_plan_s {
   bool fused = false;
   float2* peerU[16] = {};
   float2* peerV[16] = {};
+  // sparse-X' schedule: this rank's X list [count | pad | entries] in the workspace, every
+  // rank's list (peer memory), forward twiddles of the m = n_az/world point azimuth DFT
+  char* sxl = nullptr;
+  uint32_t sx_cap = 0;
+  char* peerL[16] = {};
+  float2* d_az_tab_m = nullptr;
+  bool sparse_used = false;         // the last cssar_ita_iterate ran the sparse-X' schedule
   void* ipc_base[16] = {};          // IPC mappings opened by this rank (closed on rebind/destroy)
   uint32_t* d_bar = nullptr;        // 1-word all-reduce used as the inter-sweep barrier (NCCL)
 };
@@ -220,6 +227,7 @@ int validate_params(const cssar_sar_params& p) {
   } while (0)
 
 constexpr int kTransportNone = 0, kTransportNccl = 1, kTransportGroup = 2;
+constexpr size_t kSxHeader = 256;               // sparse-X' list header (entry count) in the workspace
 
 // NCCL entry points resolved at run time from the process's libnccl.so.2 (the one torch
 // loaded, or CSSAR_NCCL_LIB); the single-GPU path never touches NCCL.
@@ -477,7 +485,7 @@ RgArgs rg_row_args(cssar_plan pl) {
 }
 
 // one ITA iteration (S1..S6) of every rank in R
-int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s) {
+int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s, bool sparse = false) {
   cssar_plan p0 = R.pl[0];
   const size_t blk = (size_t)p0->nrow * (size_t)p0->ncol * sizeof(float2);
   void *U[16], *V[16], *B[16];
@@ -529,8 +537,57 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s)
     }
     return CSSAR_OK;
   };
+  // sparse-X' S1 (sparse.cu): compact X = E(b) into a list, all ranks'
+  // lists folded into a length n_az/world array, m-point azimuth DFT -> cyclic row slab
+  auto sx_s1 = [&]() -> int {
+    for (int i = 0; i < R.np; ++i) {
+      cssar_plan pl = R.pl[i];
+      CUDA_TRY(launch_sx_compact(pl->bcol, pl->p.n_az * pl->ncol, ilog2_exact(pl->ncol), (int)(pl->rank * pl->ncol),
+                                 pl->d_st, prm.thr, reinterpret_cast<SxEntry*>(pl->sxl + kSxHeader),
+                                 reinterpret_cast<uint32_t*>(pl->sxl), pl->sx_cap, pl->sm_count, s));
+    }
+    int rc = barrier();                       // every rank's list complete
+    if (rc != CSSAR_OK) return rc;
+    for (int i = 0; i < R.np; ++i) {
+      cssar_plan pl = R.pl[i];
+      SxLists L{};
+      for (int q = 0; q < pl->world; ++q) {
+        L.list[q] = reinterpret_cast<const SxEntry*>(pl->peerL[q] + kSxHeader);
+        L.count[q] = reinterpret_cast<const uint32_t*>(pl->peerL[q]);
+      }
+      L.cap = pl->sx_cap;
+      L.world = pl->world;
+      const int n_rg = (int)pl->p.n_rg;
+      CUDA_TRY(launch_sx_fold(L, pl->rank, pl->log_naz, (int)pl->nrow, n_rg, pl->Vrow, pl->sm_count, s));
+      AzArgs a{};
+      a.tw = pl->d_az_tab_m;
+      a.n_rg = n_rg;
+      a.mask_words = n_rg / 32;
+      a.scale = (float)(1.0 / std::sqrt((double)pl->p.n_az));
+      a.oscale = (float)(1.0 / (std::sqrt((double)pl->p.n_az) * (double)n_rg));
+      a.in = pl->Vrow;
+      a.out = pl->Vrow;
+      CUDA_TRY(launch_az(ilog2_exact(pl->nrow), AZ_FWD_PLAIN, n_rg, a, s));
+      RgArgs r = rg_row_args(pl);             // S2 on the cyclic slab, plain row-major
+      r.row_base = pl->rank;
+      r.row_step = pl->world;
+      r.log_w = pl->log_nrg;
+      r.blk = 1;                              // blocked path (fused stores); j >> log_w = 0
+      r.dlog_w = ilog2_exact(pl->ncol);
+      for (int q = 0; q < pl->world; ++q) r.dst[q] = pl->peerU[q];
+      CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->nrow, r, s));
+    }
+    return CSSAR_OK;
+  };
 #define STEP(x) do { int _rc = (x); if (_rc != CSSAR_OK) return _rc; } while (0)
-  if (fused) {                                // compute + transpose in one kernel per sweep
+  if (fused && sparse) {
+    STEP(sx_s1());                            // S1' + S2: lists -> cyclic row slab -> column slabs
+    STEP(barrier());
+    STEP(az(AZ_RESID));
+    STEP(barrier());
+    STEP(rg(false));
+    STEP(barrier());
+  } else if (fused) {                         // compute + transpose in one kernel per sweep
     STEP(az(AZ_FWD_THR));                     // S1: column slabs -> every rank's row slab
     STEP(barrier());
     STEP(rg(true));                           // S2: row slab -> every rank's column slab
@@ -659,6 +716,7 @@ int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
   if ((prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && pl->world != 1) return CSSAR_ERR_INVALID_PARAMS;
   if (!(prm->tol >= 0.0) || !std::isfinite(prm->tol) || (prm->tol > 0.0 && pl->world != 1))
     return CSSAR_ERR_INVALID_PARAMS;
+  if ((prm->flags & CSSAR_FLAG_SPARSE_X) && pl->world == 1) return CSSAR_ERR_INVALID_PARAMS;
   return CSSAR_OK;
 }
 
@@ -672,15 +730,26 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
     CUDA_TRY(launch_init_state(R.pl[i]->d_st, R.pl[i]->d_hist, R.pl[i]->d_hist_full, prm.thr, sigma_fixed, s));
   int rc = setup_multi(R, Y, mask, X, s);
   if (rc != CSSAR_OK) return rc;
-  if (prm.iters > 0) {
+  // sparse-X' (CSSAR_FLAG_SPARSE_X): X_0 is arbitrary, so iteration 0 runs the dense schedule
+  // outside the graph; X_i (i >= 1) has at most k nonzeros
+  const bool sparse = (prm.flags & CSSAR_FLAG_SPARSE_X) && prm.rule == CSSAR_RULE_KSPARSE && p0->fused &&
+                      p0->d_az_tab_m && (uint64_t)prm.k <= (uint64_t)p0->sx_cap;
+  p0->sparse_used = sparse;
+  int first = 0;
+  if (sparse && prm.iters > 0) {
+    rc = iteration_multi(R, prm, s, false);
+    if (rc != CSSAR_OK) return rc;
+    first = 1;
+  }
+  if (prm.iters > first) {
     GraphKey key{nullptr, (const void*)(uintptr_t)p0->have_mask, nullptr, prm.thr, prm.rule,
-                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu, 0};
+                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu, sparse ? CSSAR_FLAG_SPARSE_X : 0};
     if (!*ghave || !(*gkey == key)) {
       if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
       *ghave = false;
       cudaGraph_t g = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(p0->cap_stream, cudaStreamCaptureModeThreadLocal));
-      rc = iteration_multi(R, prm, p0->cap_stream);
+      rc = iteration_multi(R, prm, p0->cap_stream, sparse);
       cudaError_t ec = cudaStreamEndCapture(p0->cap_stream, &g);
       if (rc != CSSAR_OK) { if (g) cudaGraphDestroy(g); return rc; }
       CUDA_TRY(ec);
@@ -690,7 +759,7 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
       *gkey = key;
       *ghave = true;
     }
-    for (int it = 0; it < prm.iters; ++it) CUDA_TRY(cudaGraphLaunch(*gexec, s));
+    for (int it = first; it < prm.iters; ++it) CUDA_TRY(cudaGraphLaunch(*gexec, s));
   }
   rc = final_multi(R, prm, X, s);
   if (rc != CSSAR_OK) return rc;
@@ -788,6 +857,7 @@ int map_peers_nccl(cssar_plan pl) {
     if (q == pl->rank) {
       pl->peerU[q] = pl->Ucol;
       pl->peerV[q] = pl->Vrow;
+      pl->peerL[q] = pl->sxl;
       continue;
     }
     void* pb = nullptr;
@@ -798,6 +868,7 @@ int map_peers_nccl(cssar_plan pl) {
     pl->ipc_base[q] = pb;
     pl->peerU[q] = reinterpret_cast<float2*>(static_cast<char*>(pb) + all[(size_t)q].off);
     pl->peerV[q] = reinterpret_cast<float2*>(reinterpret_cast<char*>(pl->peerU[q]) + voff);
+    pl->peerL[q] = reinterpret_cast<char*>(pl->peerU[q]) + (pl->sxl - reinterpret_cast<char*>(pl->Ucol));
   }
   // all ranks must agree on the mode: all-reduce the failure flag
   uint32_t bad = every ? 0u : 1u;
@@ -878,6 +949,14 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
+  if (world > 1 && pl->log_naz - ilog2_exact(world) >= 7 &&
+      (cudaMalloc(&pl->d_az_tab_m, sizeof(float2) * (az_table_count(pl->log_naz - ilog2_exact(world), false) + 2)) !=
+           cudaSuccess ||
+       az_table_fill(pl->log_naz - ilog2_exact(world), false, pl->d_az_tab_m, pl->cap_stream) != cudaSuccess ||
+       cudaStreamSynchronize(pl->cap_stream) != cudaSuccess)) {
+    cssar_plan_destroy(pl);
+    return CSSAR_ERR_CUDA;
+  }
   if (world > 1 && (cudaMalloc(&pl->d_bar, 16) != cudaSuccess || cudaMemset(pl->d_bar, 0, 16) != cudaSuccess)) {
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
@@ -900,10 +979,14 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
 
 // workspace layout: world 1: [U | cand]; world > 1: [Ucol | Vrow | Ycol | bcol | mcol | cand]
+// sparse-X' list of a world > 1 rank: kSxHeader-byte header (count) + nl/8 entries of 16 bytes
+size_t sx_bytes(size_t nl) { return align256(kSxHeader + sizeof(SxEntry) * (nl / 8)); }
+
 size_t workspace_bytes(cssar_plan pl) {
   if (pl->world == 1) return 3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
-  return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + sizeof(uint32_t) * cand_capacity((long long)nl) + 256;
+  return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + align256(sizeof(uint32_t) * cand_capacity((long long)nl)) +
+         256 + sx_bytes(nl) + 256;
 }
 
 void bind_views(cssar_plan pl, char* ws) {
@@ -924,6 +1007,8 @@ void bind_views(cssar_plan pl, char* ws) {
   pl->mcol = (uint32_t*)(ws + 4 * a);
   pl->cand = (uint32_t*)(ws + 4 * a + align256(nl / 8));
   pl->cand_cap = (uint32_t)cand_capacity((long long)nl);
+  pl->sxl = ws + 4 * a + align256(nl / 8) + align256(sizeof(uint32_t) * cand_capacity((long long)nl)) + 256;
+  pl->sx_cap = (uint32_t)(nl / 8);
   pl->U = pl->Ucol;
 }
 
@@ -974,6 +1059,7 @@ int cssar_plan_destroy(cssar_plan pl) {
   if (pl->h_conv) cudaFreeHost(pl->h_conv);
   cudaFree(pl->d_az_tab);
   cudaFree(pl->d_az_tab_r);
+  cudaFree(pl->d_az_tab_m);
   cudaFree(pl->d_st);
   cudaFree(pl->d_hist);
   cudaFree(pl->d_hist_full);
@@ -1052,14 +1138,17 @@ int cssar_group_ita_iterate(cssar_group g, const void* const* Y, const uint32_t*
     if (mask_bits[r] && !aligned16(mask_bits[r])) return CSSAR_ERR_ALIGNMENT;
     if (!g->pl[(size_t)r]->Ucol) return CSSAR_ERR_WORKSPACE;
   }
+  const bool fused = std::getenv("CSSAR_MULTI_A2A") == nullptr;
+  for (int r = 0; r < P; ++r) if (g->pl[(size_t)r]->fused != fused) g->ghave = false;
+  for (int r = 0; r < P; ++r) g->pl[(size_t)r]->fused = fused;
   const int v = validate_ita(g->pl[0], prm);
   if (v != CSSAR_OK) return v;
-  const bool fused = std::getenv("CSSAR_MULTI_A2A") == nullptr;
   for (int r = 0; r < P; ++r) {
     cssar_plan pl = g->pl[(size_t)r];
     for (int q = 0; q < P; ++q) {
       pl->peerU[q] = g->pl[(size_t)q]->Ucol;
       pl->peerV[q] = g->pl[(size_t)q]->Vrow;
+      pl->peerL[q] = g->pl[(size_t)q]->sxl;
     }
     if (pl->fused != fused) { g->ghave = false; }
     pl->fused = fused;

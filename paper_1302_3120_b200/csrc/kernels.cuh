@@ -106,6 +106,10 @@ struct RgArgs {
   // RDA with a recorded pulse (NEXT-4): G's range filter H(f_l) in fftfreq order (M uses
   // conj H) instead of the chirp P_tau quadratic q[1]; nullptr = chirp
   const float2* hrange;
+  // sparse-X' schedule (multi-GPU): local row rr is global Doppler bin row_base + rr*row_step
+  // (0 = 1), and the fused destination slabs are 2^dlog_w gates wide (0 = log_w)
+  int row_step;
+  int dlog_w;
 };
 
 enum AzMode : int {
@@ -142,6 +146,18 @@ cudaError_t launch_lambda_step(SelState* st, int thr, float mu, IterLogDev* log,
 // adaptive step: mu_i = mu_num/mu_den (1 if either is 0); b <- E(b; sigma_{i-1}) + mu_i D; histogram /
 // candidates / fixed-lambda support exactly as the tail kernel
 cudaError_t launch_adaptive_step(const AzArgs& a, long long n, int sm_count, cudaStream_t s);
+// sparse-X' schedule (multi-GPU; sparse.cu)
+struct SxEntry { int row, col; float2 v; };          // global row, global gate, X value
+struct SxLists {
+  const SxEntry* list[16];                            // every rank's list (peer memory)
+  const uint32_t* count[16];                          // every rank's entry count
+  uint32_t cap;
+  int world;
+};
+cudaError_t launch_sx_compact(const float2* b, long long n, int log_ncol, int col0, const SelState* st, int thr,
+                              SxEntry* list, uint32_t* count, uint32_t cap, int sm_count, cudaStream_t s);
+cudaError_t launch_sx_fold(const SxLists& L, int p, int log_n, int m, int n_rg, float2* F, int sm_count,
+                           cudaStream_t s);
 // tolerance stop (NEXT-4): per-block (||E(b; sigma) - Xk||^2, ||Xk||^2) into part[blocks], Xk <- E(b; sigma)
 cudaError_t launch_conv_check(const float2* b, float2* Xk, long long n, const SelState* st, int thr, double2* part,
                               int blocks, cudaStream_t s);

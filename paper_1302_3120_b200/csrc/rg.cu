@@ -140,13 +140,17 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   float2* __restrict__ data = a.data;
   constexpr int LR0 = En::template lr<false>(0), LRL = En::template lr<false>(En::P - 1);
 
+  // global Doppler bin of local row rr: row_base + rr * row_step (contiguous slabs: step 1;
+  // the sparse-X' schedule's cyclic slabs: base = rank, step = world)
+  const int rstep = a.row_step ? a.row_step : 1;
+  auto grow = [&](int rr) -> int { return a.row_base + rr * rstep; };
   float2 v[En::E];
   static_assert(En::E == 32 && C::T * 32 == N * C::B, "RCMC chunking: 32 consecutive gates per thread");
   // RDA: RCMC of the staged rows (s[b N + rsw(i)]) -> v in the first-pass group layout
   auto rcmc_apply = [&](auto tr_tag, float2* sm, float2 (&vv)[En::E], int tt) {
     constexpr bool TR = decltype(tr_tag)::value;
     const int g = tt * 32, bb = g >> LOGN, k0 = g & (N - 1);
-    rcmc_chunk<N, TR>(sm + bb * N, a.rcmc[a.row_base + row0 + bb], k0, vv);
+    rcmc_chunk<N, TR>(sm + bb * N, a.rcmc[grow(row0 + bb)], k0, vv);
     constexpr int NF = kRcmcWrapLo + kRcmcWrapHi, SL = C::B * NF, PER = (SL + C::T - 1) / C::T;
     float2 fx[TR ? PER : 1];
     if constexpr (TR) {
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
         if (f < SL) {
           const int fb = f / NF, sl = f % NF;
           const int k = sl < kRcmcWrapLo ? sl : N - NF + sl;
-          fx[q] = rcmc_T_exact<N>(sm + fb * N, a.rcmc[a.row_base + row0 + fb], k);
+          fx[q] = rcmc_T_exact<N>(sm + fb * N, a.rcmc[grow(row0 + fb)], k);
         }
       }
     }
@@ -199,12 +203,12 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   __syncthreads();                                                        // tables visible
   if constexpr (!RDA) {
     En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // prologue phase
-      const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 2 : 0];
+      const Quad q = a.coef[grow(row0 + b)].q[GBODY ? 2 : 0];
       phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     });
   } else if constexpr (GBODY) {
     En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage the row
-      phase_apply<R0, N / R0, true>(tab, a.coef[a.row_base + row0 + b].q[2], j - N / 2, x);
+      phase_apply<R0, N / R0, true>(tab, a.coef[grow(row0 + b)].q[2], j - N / 2, x);
 #pragma unroll
       for (int r = 0; r < R0; ++r) s[b * N + rsw(j + r * (N / R0))] = x[r];
     });
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   En::template passes_from<-1, false, 0>(s, v, t, tw);                   // range FFT
   auto mid_quad = [&]() {
     En::template for_groups<LRL>(v, t, [&](int b, int j, float2* x) {
-      const Quad q = a.coef[a.row_base + row0 + b].q[1];
+      const Quad q = a.coef[grow(row0 + b)].q[1];
       // bins j + r N/RL: r < RL/2 -> l' = i ; r >= RL/2 -> l' = i - N (fftfreq order, R9)
       phase_apply<RL / 2, N / RL, GBODY>(tab, q, j, x);
       phase_apply<RL / 2, N / RL, GBODY>(tab, q, j - N / 2, x + RL / 2);
@@ -247,19 +251,20 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   }
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
     if constexpr (!RDA) {
-      const Quad q = a.coef[a.row_base + row0 + b].q[GBODY ? 0 : 2];
+      const Quad q = a.coef[grow(row0 + b)].q[GBODY ? 0 : 2];
       phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     } else if constexpr (!GBODY) {
-      phase_apply<R0, N / R0, false>(tab, a.coef[a.row_base + row0 + b].q[2], j - N / 2, x);   // P_eta
+      phase_apply<R0, N / R0, false>(tab, a.coef[grow(row0 + b)].q[2], j - N / 2, x);   // P_eta
     }
     if constexpr (BLK) {
       if (a.dst[0]) {                      // fused transpose: straight into the ranks' column slabs
-        const int wm = (1 << a.log_w) - 1;
-        const size_t rowoff = (size_t)((a.drank << a.dlog_nrow) + row0 + b) << a.log_w;
+        const int dlw = a.dlog_w ? a.dlog_w : a.log_w;         // column-slab width of the destinations
+        const int wm = (1 << dlw) - 1;
+        const size_t rowoff = (size_t)grow(row0 + b) << dlw;
 #pragma unroll
         for (int r = 0; r < R0; ++r) {
           const int jj = j + r * (N / R0);
-          a.dst[jj >> a.log_w][rowoff + (size_t)(jj & wm)] = x[r];
+          a.dst[jj >> dlw][rowoff + (size_t)(jj & wm)] = x[r];
         }
         return;
       }

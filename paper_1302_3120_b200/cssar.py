@@ -33,6 +33,7 @@ SYMBOLS = [
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
+CSSAR_FLAG_SPARSE_X = 4
 STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
 
 
@@ -228,7 +229,7 @@ class Plan:
         return out
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
-                    log=False, profile_stages=False, stream=None, tol=0.0):
+                    log=False, profile_stages=False, stream=None, tol=0.0, sparse=False):
         """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X.
         mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU).  tol > 0: stop after the
         first update with ||X_(i+1) - X_i|| <= tol ||X_i|| (self.iters_done = updates performed)."""
@@ -241,7 +242,8 @@ class Plan:
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
                          int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
                          (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
-                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0), float(tol))
+                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0) | (CSSAR_FLAG_SPARSE_X if sparse else 0),
+                         float(tol))
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
                                         logbuf if log else None, _stream(stream))
@@ -349,14 +351,17 @@ class Group:
             pass
 
     def ita_iterate(self, Ys, mask_bits, Xs, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, log=False,
-                    stream=None):
-        """Ys, Xs: lists of row-slab tensors (rank order); mask_bits: list or None."""
+                    stream=None, sparse=False):
+        """Ys, Xs: lists of row-slab tensors (rank order); mask_bits: list or None.
+        sparse=True: the sparse-X' schedule (CSSAR_FLAG_SPARSE_X)."""
         W = self.world
         arr = ctypes.c_void_p * W
         ys = arr(*[_ptr(y) for y in Ys])
         ms = arr(*([_ptr(m) for m in mask_bits] if mask_bits is not None else [None] * W))
         xs = arr(*[_ptr(x) for x in Xs])
         prm = _itaprm(thr, rule, k, lam, mu, iters)
+        if sparse:
+            prm.flags |= CSSAR_FLAG_SPARSE_X
         logbuf = (IterLogC * max(1, iters))() if log else None
         _check(self.lib.cssar_group_ita_iterate(self.h, ys, ms, ctypes.byref(prm), xs, logbuf if log else None,
                                                 _stream(stream)), "cssar_group_ita_iterate")

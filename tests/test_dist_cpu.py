@@ -151,3 +151,22 @@ def test_slab_schedule_two_ranks_gloo():
         assert out["G_err"] <= 1e-12, (r, out["G_err"])
         for k, (val_ok, above_ok) in out["select"].items():
             assert val_ok and above_ok, (r, k)
+
+
+def test_sparse_x_fold_identity():
+    """The sparse-X' decomposition (api.cu sx_s1, sparse.cu): with N = P m and n = m n1 + n2,
+    F_p[n2] = sum_{n = n2 mod m} w_N^{p n} x[n] and the m-point DFT of F_p gives bins p + P k2
+    of the N-point DFT, for every rank p (numpy, fp64)."""
+    import numpy as np
+    rng = np.random.default_rng(7)
+    N, P, cols = 256, 8, 5
+    m = N // P
+    x = np.zeros((N, cols), complex)
+    idx = rng.choice(N * cols, 40, replace=False)
+    x.reshape(-1)[idx] = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    ref = np.fft.fft(x, axis=0)
+    n = np.arange(N)
+    for p in range(P):
+        F = np.zeros((m, cols), complex)
+        np.add.at(F, n % m, np.exp(-2j * np.pi * p * n / N)[:, None] * x)
+        assert np.abs(np.fft.fft(F, axis=0) - ref[p::P]).max() < 1e-10

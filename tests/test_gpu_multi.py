@@ -118,3 +118,75 @@ def test_world_validation():
     assert e.value.code == -2
     with pytest.raises(CssarError):
         Group(configs.get("c1").params, 32)  # world > 16
+
+
+# ---- sparse-X' schedule (CSSAR_FLAG_SPARSE_X)
+@pytest.mark.parametrize("name,grid,world,iters", [
+    ("c1", None, 2, 12),
+    ("c1", None, 4, 12),
+    ("c2", (1024, 1024), 4, 8),
+    ("c3", (2048, 1024), 8, 6),     # line mask; k <= n_az n_rg / (8 world) sets the world
+])
+def test_group_sparse_x_matches_single_gpu(name, grid, world, iters):
+    """From iteration 1 on S1 + transpose #1 are replaced by the compacted X' (all-gathered
+    over peer memory), a fold into n_az/world cyclic Doppler bins and a local m-point DFT.
+    Not bitwise (another factorisation, atomic folds): X within 1e-5 of world 1, the same
+    thresholds and support sizes."""
+    import torch
+    from paper_1302_3120_b200 import Group
+    prob = problem(name, *(grid or (None, None)))
+    cfg = prob.cfg
+    Xs, ls = _single_run(prob, iters)
+    g = Group(cfg.params, world)
+    Ys = [to_dev(y) for y in _slabs(prob.Y, world)]
+    Ms = [m.contiguous() for m in _slabs(mask_bits_dev(prob.mask), world)]
+    Xg = [torch.zeros_like(y) for y in Ys]
+    lg = g.ita_iterate(Ys, Ms, Xg, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=iters, log=True,
+                       sparse=True)
+    Xg = np.concatenate([to_host(x) for x in Xg], axis=0)
+    assert rel_l2(Xg, Xs) <= 1e-5, rel_l2(Xg, Xs)
+    sg = np.array([e["sigma"] for e in lg])
+    ss = np.array([e["sigma"] for e in ls])
+    assert np.max(np.abs(sg - ss) / ss) <= 1e-5
+    assert [e["support"] for e in lg] == [e["support"] for e in ls]
+
+
+def test_group_sparse_x_matches_oracle_c1():
+    prob = problem("c1", iters=30)
+    cfg = prob.cfg
+    op = csa.CSAOperator(cfg.params)
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu,
+                 iters=30)
+    import torch
+    from paper_1302_3120_b200 import Group
+    g = Group(cfg.params, 4)
+    Ys = [to_dev(y) for y in _slabs(prob.Y, 4)]
+    Ms = [m.contiguous() for m in _slabs(mask_bits_dev(prob.mask), 4)]
+    Xg = [torch.zeros_like(y) for y in Ys]
+    g.ita_iterate(Ys, Ms, Xg, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=30, sparse=True)
+    Xg = np.concatenate([to_host(x) for x in Xg], axis=0)
+    assert rel_l2(Xg, Xo) <= 1e-3
+    assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
+
+
+def test_sparse_x_flag_falls_back_where_it_does_not_apply(monkeypatch):
+    """The flag is a request: world 1 rejects it; fixed lambda, the all-to-all transport and
+    k above the list capacity run the dense schedule (bitwise the plain group result)."""
+    import torch
+    from paper_1302_3120_b200 import Group, Plan, CssarError
+    prob = problem("c2", 512, 512)
+    cfg = prob.cfg
+    with pytest.raises(CssarError) as e:
+        Plan(cfg.params).ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), k=cfg.k, iters=2, sparse=True)
+    assert e.value.code == -1
+    g = Group(cfg.params, 2)
+    Ys = [to_dev(y) for y in _slabs(prob.Y, 2)]
+
+    def run(**kw):
+        Xg = [torch.zeros_like(y) for y in Ys]
+        g.ita_iterate(Ys, None, Xg, iters=3, **kw)
+        return np.concatenate([to_host(x) for x in Xg], axis=0)
+    for kw in (dict(rule="lambda", lam=0.1), dict(k=200000)):
+        assert np.array_equal(run(sparse=True, **kw), run(**kw))
+    monkeypatch.setenv("CSSAR_MULTI_A2A", "1")
+    assert np.array_equal(run(sparse=True, k=cfg.k), run(k=cfg.k))
