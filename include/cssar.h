@@ -141,9 +141,10 @@ typedef struct cssar_plan_s* cssar_plan;
  *     on one rank, distributed by the caller; the plan creates its own NCCL communicator
  *     (collective call: every rank must call it; NCCL from the process's libnccl.so.2).
  *     world must divide n_az and n_rg with n_rg/world >= 128 and n_az/world a multiple of
- *     the range kernel's rows per CTA; else CSSAR_ERR_UNSUPPORTED_SIZE.  Only
- *     cssar_ita_iterate (the hot path) runs on world > 1 plans; the single-array operator
- *     calls and debug hooks return CSSAR_ERR_BAD_PLAN.  NCCL failures: CSSAR_ERR_NCCL. */
+ *     the range kernel's rows per CTA; else CSSAR_ERR_UNSUPPORTED_SIZE.  cssar_ita_iterate
+ *     and the operators cssar_forward / cssar_adjoint / cssar_image take this rank's row
+ *     slabs and are collective over the ranks (needs a bound workspace); the debug hooks
+ *     return CSSAR_ERR_BAD_PLAN.  NCCL failures: CSSAR_ERR_NCCL. */
 int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int rank,
                       const void* nccl_unique_id, void* stream);
 int cssar_plan_destroy(cssar_plan plan);
@@ -165,7 +166,9 @@ int cssar_workspace_size(cssar_plan plan, size_t* bytes);
  * transposes (also forced by the environment variable CSSAR_MULTI_A2A). */
 int cssar_bind_workspace(cssar_plan plan, void* ws, size_t bytes);
 
-/* Y_out = Theta o G(X)   (A X, eq. 24).  X and Y_out may alias. */
+/* Y_out = Theta o G(X)   (A X, eq. 24).  X and Y_out may alias.  world > 1: row slabs in and
+ * out, collective (column-slab azimuth sweeps, two all-to-all transposes around the range
+ * sweep; the workspace must be bound), bitwise equal to world 1. */
 int cssar_forward(cssar_plan plan, const void* X, const uint32_t* mask_bits, void* Y_out, void* stream);
 /* X_out = M(Theta o R)   (A^H R).  R and X_out may alias. */
 int cssar_adjoint(cssar_plan plan, const void* R, const uint32_t* mask_bits, void* X_out, void* stream);
@@ -222,6 +225,11 @@ int cssar_group_bind_workspace(cssar_group group, int rank, void* ws, size_t byt
 int cssar_group_ita_iterate(cssar_group group, const void* const* Y, const uint32_t* const* mask_bits,
                             const cssar_ita_params* prm, void* const* X_inout, cssar_iter_log* log_host,
                             void* stream);
+/* The single-device emulation of cssar_forward (forward = 1) / cssar_adjoint = cssar_image
+ * (forward = 0) on world > 1 row slabs: in, mask_bits (entries NULL = all ones), out are
+ * arrays of `world` device pointers. */
+int cssar_group_operator(cssar_group g, int forward, const void* const* in, const uint32_t* const* mask_bits,
+                         void* const* out, void* stream);
 
 /* ---- test hooks (parity of single sweeps / the select; not needed by users) ---------- */
 /* One range sweep in place on a (Doppler, range-time) array: gbody=1 -> Phi3* F Phi2* F^-1

@@ -721,6 +721,67 @@ int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
 }
 
 // the whole multi-rank solve for the ranks in R (NCCL rank or emulation group)
+// forward / adjoint / image on world > 1 plans (the boundary's "local slab" contract, SURVEY
+// 8(b)): input row slabs -> column slabs (pack + all-to-all), first azimuth sweep, all-to-all
+// into blocked row slabs, range sweep, all-to-all back, second azimuth sweep, column slabs ->
+// output row slabs.  Same kernels and global indices as world 1 (bitwise equal results).
+int op_multi(const Ranks& R, bool forward, const void* const* in, const uint32_t* const* mask, void* const* out,
+             cudaStream_t s) {
+  cssar_plan p0 = R.pl[0];
+  for (int i = 0; i < R.np; ++i)
+    if (!R.pl[i]->Ucol) return CSSAR_ERR_WORKSPACE;
+  const size_t n_rg = (size_t)p0->p.n_rg;
+  const size_t blk = (size_t)p0->nrow * (size_t)p0->ncol * sizeof(float2);
+  void *U[16], *V[16], *Bc[16], *Mc[16];
+  gather_ptrs(R, U, [](cssar_plan q) { return q->Ucol; });
+  gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
+  gather_ptrs(R, Bc, [](cssar_plan q) { return q->bcol; });
+  gather_ptrs(R, Mc, [](cssar_plan q) { return q->mcol; });
+  int rc;
+  const bool have_mask = mask[0] != nullptr;
+  for (int i = 0; i < R.np; ++i) R.pl[i]->have_mask = have_mask;
+  if (have_mask) {
+    for (int i = 0; i < R.np; ++i)
+      if ((rc = pack_rows(R.pl[i], mask[i], R.pl[i]->Vrow, n_rg / 32, sizeof(uint32_t), s)) != CSSAR_OK) return rc;
+    if ((rc = xchg_a2a(R, V, Mc, (size_t)p0->nrow * (size_t)(p0->ncol / 32) * sizeof(uint32_t), s)) != CSSAR_OK)
+      return rc;
+  }
+  for (int i = 0; i < R.np; ++i)
+    if ((rc = pack_rows(R.pl[i], in[i], R.pl[i]->Vrow, n_rg, sizeof(float2), s)) != CSSAR_OK) return rc;
+  if ((rc = xchg_a2a(R, V, Bc, blk, s)) != CSSAR_OK) return rc;
+  cssar_ita_params prm{};
+  prm.thr = CSSAR_THR_SOFT;
+  prm.rule = CSSAR_RULE_KSPARSE;
+  prm.mu = 1.0;
+  for (int i = 0; i < R.np; ++i) {                        // F_eta (forward: plain; adjoint: Theta first)
+    cssar_plan pl = R.pl[i];
+    AzArgs a = az_col_args(pl, prm);
+    a.in = pl->bcol;
+    a.out = pl->Ucol;
+    if (forward) a.mask = nullptr;
+    CUDA_TRY(launch_az(pl->log_naz, forward ? AZ_FWD_PLAIN : AZ_FWD_MASK, a.n_rg, a, s));
+  }
+  if ((rc = xchg_a2a(R, U, V, blk, s)) != CSSAR_OK) return rc;
+  for (int i = 0; i < R.np; ++i) {                        // range body (G or M) on blocked row slabs
+    cssar_plan pl = R.pl[i];
+    RgArgs r = rg_row_args(pl);
+    CUDA_TRY(launch_rg_sweep(pl->log_nrg, forward, (int)pl->nrow, r, s));
+  }
+  if ((rc = xchg_a2a(R, V, U, blk, s)) != CSSAR_OK) return rc;
+  for (int i = 0; i < R.np; ++i) {                        // F_eta^-1 (forward: then Theta)
+    cssar_plan pl = R.pl[i];
+    AzArgs a = az_col_args(pl, prm);
+    a.in = pl->Ucol;
+    a.out = pl->bcol;
+    if (!forward) a.mask = nullptr;
+    CUDA_TRY(launch_az(pl->log_naz, forward ? AZ_INV_MASK : AZ_INV_PLAIN, a.n_rg, a, s));
+  }
+  if ((rc = xchg_a2a(R, Bc, V, blk, s)) != CSSAR_OK) return rc;
+  for (int i = 0; i < R.np; ++i)
+    if ((rc = unpack_rows(R.pl[i], R.pl[i]->Vrow, out[i], n_rg, sizeof(float2), s)) != CSSAR_OK) return rc;
+  return CSSAR_OK;
+}
+
 int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask, const cssar_ita_params& prm,
               void* const* X, cssar_iter_log* log_host, cudaStream_t s, cudaGraphExec_t* gexec, GraphKey* gkey,
               bool* ghave) {
@@ -1159,15 +1220,36 @@ int cssar_group_ita_iterate(cssar_group g, const void* const* Y, const uint32_t*
 }
 
 int cssar_forward(cssar_plan pl, const void* X, const uint32_t* mask_bits, void* Y_out, void* stream) {
-  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
+  if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(X) || !aligned16(Y_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
+  if (pl->world > 1) {
+    Ranks R{&pl, 1};
+    return op_multi(R, true, &X, &mask_bits, &Y_out, (cudaStream_t)stream);
+  }
   return enqueue_forward(pl, X, mask_bits, Y_out, (cudaStream_t)stream);
 }
 
 int cssar_adjoint(cssar_plan pl, const void* R, const uint32_t* mask_bits, void* X_out, void* stream) {
-  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
+  if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(R) || !aligned16(X_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
+  if (pl->world > 1) {
+    Ranks Rk{&pl, 1};
+    return op_multi(Rk, false, &R, &mask_bits, &X_out, (cudaStream_t)stream);
+  }
   return enqueue_adjoint(pl, R, mask_bits, X_out, (cudaStream_t)stream);
+}
+
+int cssar_group_operator(cssar_group g, int forward, const void* const* in, const uint32_t* const* mask_bits,
+                         void* const* out, void* stream) {
+  if (!g || g->pl.empty() || !in || !mask_bits || !out) return CSSAR_ERR_BAD_PLAN;
+  const int P = (int)g->pl.size();
+  for (int r = 0; r < P; ++r) {
+    if (!aligned16(in[r]) || !aligned16(out[r])) return CSSAR_ERR_ALIGNMENT;
+    if ((mask_bits[r] != nullptr) != (mask_bits[0] != nullptr)) return CSSAR_ERR_INVALID_PARAMS;
+    if (mask_bits[r] && !aligned16(mask_bits[r])) return CSSAR_ERR_ALIGNMENT;
+  }
+  Ranks R{g->pl.data(), P};
+  return op_multi(R, forward != 0, in, mask_bits, out, (cudaStream_t)stream);
 }
 
 int cssar_image(cssar_plan pl, const void* Y, const uint32_t* mask_bits, void* X_out, void* stream) {

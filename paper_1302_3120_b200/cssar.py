@@ -29,7 +29,7 @@ SYMBOLS = [
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
     "cssar_debug_fallbacks", "cssar_stage_times", "cssar_nccl_unique_id", "cssar_group_create",
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
-    "cssar_ita_iters_done", "cssar_plan_set_pulse",
+    "cssar_ita_iters_done", "cssar_plan_set_pulse", "cssar_group_operator",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
@@ -97,6 +97,7 @@ def load_library(path=None):
     lib.cssar_group_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
     lib.cssar_ita_iters_done.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.cssar_plan_set_pulse.argtypes = [P, V, I64]
+    lib.cssar_group_operator.argtypes = [P, I, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(V), V]
     lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
     lib.cssar_group_ita_iterate.argtypes = [P, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(ItaParamsC),
                                             ctypes.POINTER(V), ctypes.POINTER(IterLogC), V]
@@ -349,6 +350,24 @@ class Group:
             self.close()
         except Exception:
             pass
+
+    def _operator(self, forward, ins, mask_bits, outs, stream):
+        W = self.world
+        arr = ctypes.c_void_p * W
+        if outs is None:
+            outs = [torch.empty(self.shape, dtype=torch.complex64, device="cuda") for _ in range(W)]
+        ms = arr(*([_ptr(m) for m in mask_bits] if mask_bits is not None else [None] * W))
+        _check(self.lib.cssar_group_operator(self.h, int(forward), arr(*[_ptr(x) for x in ins]), ms,
+                                             arr(*[_ptr(y) for y in outs]), _stream(stream)), "cssar_group_operator")
+        return outs
+
+    def forward(self, Xs, mask_bits=None, outs=None, stream=None):
+        """Row slabs of Theta o G(X) (cssar_forward on world ranks)."""
+        return self._operator(True, Xs, mask_bits, outs, stream)
+
+    def adjoint(self, Rs, mask_bits=None, outs=None, stream=None):
+        """Row slabs of M(Theta o R) (cssar_adjoint / cssar_image on world ranks)."""
+        return self._operator(False, Rs, mask_bits, outs, stream)
 
     def ita_iterate(self, Ys, mask_bits, Xs, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, log=False,
                     stream=None, sparse=False):

@@ -190,3 +190,28 @@ def test_sparse_x_flag_falls_back_where_it_does_not_apply(monkeypatch):
         assert np.array_equal(run(sparse=True, **kw), run(**kw))
     monkeypatch.setenv("CSSAR_MULTI_A2A", "1")
     assert np.array_equal(run(sparse=True, k=cfg.k), run(k=cfg.k))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_group_operators_bitwise_single_gpu(world):
+    """cssar_forward / cssar_adjoint on world > 1 row slabs (collective): bitwise equal to one
+    GPU, which is pinned to the oracle in test_gpu_ops.py; one case checked against the oracle."""
+    from paper_1302_3120_b200 import Group, Plan
+    from tests._common import rand_c
+    p = configs.get("c1").params
+    X = rand_c((p.n_az, p.n_rg), 41)
+    mask = (np.random.default_rng(42).random((p.n_az, p.n_rg)) < 0.4).astype(np.uint8)
+    mb = mask_bits_dev(mask)
+    pl = Plan(p)
+    fs = to_host(pl.forward(to_dev(X), mb))
+    as_ = to_host(pl.adjoint(to_dev(X), mb))
+    g = Group(p, world)
+    Xs = [to_dev(x) for x in _slabs(X, world)]
+    Ms = [m.contiguous() for m in _slabs(mb, world)]
+    fg = np.concatenate([to_host(y) for y in g.forward(Xs, Ms)], axis=0)
+    ag = np.concatenate([to_host(y) for y in g.adjoint(Xs, Ms)], axis=0)
+    assert np.array_equal(fg.view(np.uint32), fs.view(np.uint32))
+    assert np.array_equal(ag.view(np.uint32), as_.view(np.uint32))
+    ig = np.concatenate([to_host(y) for y in g.adjoint(Xs, None)], axis=0)
+    op = csa.CSAOperator(p)
+    assert rel_l2(ig, op.M(X.astype(np.complex128))) <= 1e-5
