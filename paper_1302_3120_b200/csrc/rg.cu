@@ -142,8 +142,10 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
 
   // global Doppler bin of local row rr: row_base + rr * row_step (contiguous slabs: step 1;
   // the sparse-X' schedule's cyclic slabs: base = rank, step = world)
-  const int rstep = a.row_step ? a.row_step : 1;
-  auto grow = [&](int rr) -> int { return a.row_base + rr * rstep; };
+  auto grow = [&](int rr) -> int {
+    if constexpr (BLK) return a.row_base + rr * (a.row_step ? a.row_step : 1);
+    else return a.row_base + rr;                                  // single GPU: contiguous rows
+  };
   float2 v[En::E];
   static_assert(En::E == 32 && C::T * 32 == N * C::B, "RCMC chunking: 32 consecutive gates per thread");
   // RDA: RCMC of the staged rows (s[b N + rsw(i)]) -> v in the first-pass group layout
