@@ -1,5 +1,6 @@
 // libcssar C ABI (include/cssar.h): plan (S0 phase-coefficient table), operator calls and
 // the graph-replayed ITA loop.  Host code only; device work lives in kernels.cu.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
@@ -243,6 +244,7 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*asyncError)(ncclComm_t, ncclResult_t*) = nullptr;   // optional
 };
 
 NcclApi load_nccl() {
@@ -263,6 +265,7 @@ NcclApi load_nccl() {
   NCCL_SYM(recv, "ncclRecv");
   NCCL_SYM(allReduce, "ncclAllReduce");
   NCCL_SYM(allGather, "ncclAllGather");
+  NCCL_SYM(asyncError, "ncclCommGetAsyncError");
 #undef NCCL_SYM
   a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv &&
          a.allReduce && a.allGather;
@@ -327,7 +330,17 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
 // one ITA iteration (S1..S6) on stream s
 int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const cssar_ita_params& prm, void* X,
                       cudaStream_t s, bool prof = false) {
-#define MARK(i) do { if (prof) CUDA_TRY(cudaEventRecord(pl->ev[i], s)); } while (0)
+  // PROFILE_STAGES: CUDA events between the steps, and NVTX ranges S1..S6 for nsys timelines
+  static const char* const kStage[6] = {"S1 az head", "S2 range G", "S3 az residual", "S4 range M", "S5 az tail",
+                                         "S6 select"};
+#define MARK(i)                                               \
+  do {                                                        \
+    if (prof) {                                               \
+      if ((i) > 0) nvtxRangePop();                            \
+      if ((i) < 6) nvtxRangePushA(kStage[(i) < 6 ? (i) : 0]); \
+      CUDA_TRY(cudaEventRecord(pl->ev[i], s));                \
+    }                                                         \
+  } while (0)
   AzArgs a{};
   a.tw = pl->d_az_tab;
   a.n_rg = (int)pl->p.n_rg;
@@ -1256,8 +1269,16 @@ int cssar_image(cssar_plan pl, const void* Y, const uint32_t* mask_bits, void* X
   return cssar_adjoint(pl, Y, mask_bits, X_out, stream);
 }
 
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, const cssar_ita_params* prm,
                       void* X_inout, cssar_iter_log* log_host, void* stream) {
+  NvtxRange nvtx_range("cssar_ita_iterate");
   if (!pl || !prm) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(Y) || !aligned16(X_inout) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
   const int v = validate_ita(pl, prm);
@@ -1267,7 +1288,13 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   pl->iters_done = prm->iters;
   if (pl->world > 1) {                          // this rank's row slabs; NCCL transposes
     Ranks R{&pl, 1};
-    return ita_multi(R, &Y, &mask_bits, *prm, &X_inout, log_host, s, &pl->gexec, &pl->gkey, &pl->ghave);
+    const int rc = ita_multi(R, &Y, &mask_bits, *prm, &X_inout, log_host, s, &pl->gexec, &pl->gkey, &pl->ghave);
+    if (rc == CSSAR_OK && pl->comm && nccl().asyncError) {     // failure detection
+      ncclResult_t ae = ncclSuccess;
+      if (nccl().asyncError(pl->comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress))
+        return CSSAR_ERR_NCCL;
+    }
+    return rc;
   }
   const float sigma_fixed = prm->rule == CSSAR_RULE_FIXED_LAMBDA ? (float)fixed_sigma(*prm) : 0.f;
   CUDA_TRY(launch_init_state(pl->d_st, pl->d_hist, pl->d_hist_full, prm->thr, sigma_fixed, s));

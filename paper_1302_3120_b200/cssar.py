@@ -134,6 +134,18 @@ def _params_c(p, op="csa"):
                       OP_CODES[op])
 
 
+def write_log_csv(entries, path):
+    """Per-iteration solver report (SPEC "SolverReport", CSV export S:L394): one row
+    per X update with sigma_i, lambda_i, mu_i, support size and ||Theta(Y - G X_i)||^2."""
+    import csv
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["iter", "sigma", "lambda", "mu", "support", "resid2"])
+        for i, e in enumerate(entries):
+            w.writerow([i, repr(float(e["sigma"])), repr(float(e["lam"])), repr(float(e["mu"])), int(e["support"]),
+                        repr(float(e["resid2"]))])
+
+
 def nccl_unique_id():
     """A fresh 128-byte ncclUniqueId (bytes) for Plan(world > 1)."""
     lib = load_library()

@@ -87,3 +87,15 @@ def test_params_validation_without_gpu():
     wide = cssar._params_c(SarParams(n_az=256, n_rg=16384, Fr=120e6, prf=4000.0), "rda")
     assert lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(wide), 1, 0, None, None) == -1
     assert not h.value
+
+
+def test_log_csv_export(tmp_path):
+    import csv
+    from paper_1302_3120_b200.cssar import write_log_csv
+    entries = [dict(sigma=1.5, lam=1.5, mu=1.0, support=5, resid2=2.25), dict(sigma=0.5, lam=0.5, mu=1.0, support=4,
+                                                                                 resid2=1.0)]
+    path = tmp_path / "log.csv"
+    write_log_csv(entries, path)
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["iter", "sigma", "lambda", "mu", "support", "resid2"]
+    assert [float(r[1]) for r in rows[1:]] == [1.5, 0.5] and rows[2][4] == "4"

@@ -361,3 +361,18 @@ def test_ita_tall_grids_every_cluster_shape(n_az, n_rg, op):
     Xg = to_host(Plan(cfg.params, op=op).ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr,
                                                        rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=4))
     assert rel_l2(Xg, Xo) <= TOL_ITA
+
+
+def test_ita_runs_are_bitwise_deterministic():
+    """SURVEY 5 (race detection): two runs give bitwise identical X and logs (the histogram
+    atomics count integers; every floating-point reduction order is fixed)."""
+    prob = problem("c1", iters=15)
+    cfg = prob.cfg
+    out = []
+    for _ in range(2):
+        pl = _plan(cfg.params)
+        X, log = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr, rule=cfg.rule, k=cfg.k,
+                                mu=cfg.mu, iters=15, log=True)
+        out.append((to_host(X), [(e["sigma"], e["support"]) for e in log]))
+    assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
+    assert out[0][1] == out[1][1]
