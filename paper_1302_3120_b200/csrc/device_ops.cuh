@@ -23,6 +23,14 @@ CSSAR_DEV uint32_t mag2_bits(float2 v) {
   return __float_as_uint(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
 }
 
+// MUFU reciprocal square root without the denormal rescaling rsqrtf() carries (a denormal
+// |b|^2 is below any sigma^2 the select can produce except 0, which the callers guard)
+CSSAR_DEV float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // E(b; sigma): strict survival on the fp32 |b|^2 pattern,
 // soft (eq. 9), half (q = 1/2), hard (q = 0) or q = 2/3 shrink of the magnitude, phase kept.
 CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
@@ -30,20 +38,20 @@ CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
   const float a2 = __uint_as_float(u);
   float f;
   if (thr == THR_SOFT) {
-    f = fmaf(-sigma, rsqrtf(a2), 1.0f);                   // 1 - sigma/|b|   (sigma = 0 -> 1)
+    f = sigma == 0.f ? 1.0f : fmaf(-sigma, rsqrt_ftz(a2), 1.0f);   // 1 - sigma/|b|
   } else if (thr == THR_HARD) {
     f = 1.0f;
   } else if (thr == THR_TWOTHIRDS) {
     // closed-form L2/3 minimiser in k-rule form (oracle/ita.py twothirds): q = 27 t^2 /
     // (16 lm^(3/2)) = (3 sqrt(3)/4)(t/sigma)^2, phi = c sigma^(1/3) sqrt(cosh(acosh(q)/3))
-    const float t = a2 * rsqrtf(a2);
+    const float t = a2 * rsqrt_ftz(a2);
     const float q = 1.2990381056766580f * a2 / (sigma * sigma);
     const float phi = 1.2061639667263164f * cbrtf(sigma) * sqrtf(coshf(acoshf(q) * (1.0f / 3.0f)));
     const float x = 0.5f * (phi + sqrtf(2.0f * t / phi - phi * phi));
     f = x * x * x / t;
     f = sigma == 0.f ? 1.0f : f;
   } else {
-    const float ratio = sigma * rsqrtf(a2);
+    const float ratio = sigma * rsqrt_ftz(a2);
     const float phi = acosf(0.70710678118654752f * ratio * sqrtf(ratio));
     f = (2.0f / 3.0f) * (1.0f + cosf(2.09439510239319549f - (2.0f / 3.0f) * phi));
     f = sigma == 0.f ? 1.0f : f;
