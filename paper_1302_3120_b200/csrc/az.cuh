@@ -64,7 +64,7 @@ struct AzCfg<13, true> {
 };
 #endif
 
-template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true>
+template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true, bool DEF = false>
 struct AzShape {
   using P = AzCfg<LOGN, R>;
   static constexpr int C = P::C, W = P::W, E = P::E, NS = NSO > 0 ? NSO : P::NS;
@@ -88,7 +88,8 @@ struct AzShape {
   static constexpr int BM = M < 256 ? M : 256;             // TMA box rows (box dims <= 256)
   static constexpr uint32_t STAGE_BYTES = (uint32_t)(sizeof(float2) * M * W);
   // RESID: + a TMA-loaded buffer of Y at the output rows k + M q ([q][k][w])
-  static constexpr size_t CL_Y_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0));
+  // DEF (deferred epilogue): a second receive buffer, the panels' pushes alternate between them
+  static constexpr size_t CL_Y_OFF = sizeof(float2) * (size_t)M * W * (NS + 1 + (R && !XS ? 1 : 0) + (DEF ? 1 : 0));
   static constexpr size_t CL_TW_OFF = CL_Y_OFF + (R ? sizeof(float2) * (size_t)M * W : 0);
   static constexpr int LO = (LOGN + 1) / 2;                      // cluster twiddle table split
   static constexpr int CTW = (1 << LO) + (1 << (LOGN - LO));      // lo[2^LO] | hi[N / 2^LO]
@@ -472,8 +473,17 @@ CSSAR_DEV void mbar_wait_cta(const uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// deferred epilogue (HEAD): panel p's cross-CTA step and stores run after panel p+1's push,
+// so the wait for the slowest peer's push overlaps a whole local transform
+#if defined(CSSAR_AZ_NO_DEFER)
+template <int MODE>
+constexpr bool kAzDefer = false;
+#else
+template <int MODE>
+constexpr bool kAzDefer = MODE == AZ_FWD_THR;
+#endif
 template <int LOGN, int MODE>
-using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, MODE == AZ_TAIL>;
+using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, MODE == AZ_TAIL, kAzDefer<MODE>>;
 
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
@@ -498,6 +508,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK ||
                       MODE == AZ_NORM;
   static_assert(C > 1, "cluster kernel");
+  constexpr bool DEFER = kAzDefer<MODE> && !RES && !AUX && !BS && NS == 1;
   using En = typename Cf::En;
   using Ops = AzOps<MODE>;
   constexpr int R0 = 1 << En::template lr<false>(0);
@@ -583,7 +594,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     mbar_init(xfull, 1u);
     mbar_init(yfull, 1u);
     mbar_expect_tx(rfull, Cf::STAGE_BYTES);        // armed for the first panel
-    if (RES) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
+    if (RES || DEFER) mbar_expect_tx(xfull, Cf::STAGE_BYTES);   // DEFER: xfull = second receive buffer
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     for (int i = 0; i < NS; ++i)
@@ -593,6 +604,39 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   // barrier initialisation visible cluster-wide before any remote st.async (once per kernel)
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
+  // DEFER: cross-CTA step, consume, arrive and stores of panel `pp` (its it index `pit`)
+  auto defer_finish = [&](int pp, int pit) {
+    if constexpr (DEFER) {
+      float2* rb = rbuf0 + ((pit & 1) ? (size_t)M * W : 0);
+      uint64_t* rbar = (pit & 1) ? xfull : rfull;
+      mbar_wait_cta(rbar, (uint32_t)((pit >> 1) & 1));
+      if (t == 0) mbar_expect_tx(rbar, Cf::STAGE_BYTES);
+      float2 z[PT][C];
+#pragma unroll
+      for (int p = 0; p < PT; p += 2) {
+        const int off = (slot_k(p) - rank * (M / C)) * W + slot_w(p);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(rb + c * (M / C) * W + off);
+          z[p][c] = make_float2(q.x, q.y);
+          z[p + 1][c] = make_float2(q.z, q.w);
+        }
+        cluster_twiddles2<C, Ops::DIR, LOGN, Cf::LO>(z[p], z[p + 1], (uint32_t)slot_k(p), ctw);
+        dft_sr<C, Ops::DIR>(z[p]);
+        dft_sr<C, Ops::DIR>(z[p + 1]);
+      }
+      consume(z, misc + 40);
+      cl_arrive();                                 // this receive buffer consumed
+      Aux ax0[C];
+      const int c0 = pp * W;
+#pragma unroll
+      for (int p = 0; p < PT; p += 2) {
+        const int w = slot_w(p), k = slot_k(p);
+#pragma unroll
+        for (int q = 0; q < C; ++q) Ops::epi2(a, k + M * q, c0 + w, z[p][q], z[p + 1][q], ax0[q], ax0[q], tc, racc);
+      }
+    }
+  };
   int it = 0;
   for (int panel = cid; panel < npan; panel += ncl, ++it) {
     const int sidx = it % NS;
@@ -600,6 +644,9 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     float2* rbuf = rbuf0;
     if constexpr (PP) {
       if (it & 1) { s = rbuf0; rbuf = stages; }
+    }
+    if constexpr (DEFER) {
+      if (it & 1) rbuf = rbuf0 + (size_t)M * W;
     }
     const int col0 = panel * W;
     const int next = panel + NS * ncl;
@@ -688,7 +735,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     // push local output k of every column to its owner rank k / (M/C): rbuf[(rank M/C + k%(M/C)) W + w]
     if (it > 0) cl_wait();                         // owners are done reading their receive buffers
     {
-      const uint32_t rb = smem_u32(rbuf), bar = smem_u32(rfull);
+      const uint32_t rb = smem_u32(rbuf), bar = smem_u32((DEFER && (it & 1)) ? xfull : rfull);
       En::template for_groups<En::template lr<false>(En::P - 1)>(v, t, [&](int w, int j, float2* x) {
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
@@ -698,6 +745,11 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           st_async_cluster(mapa(rb + off, own), x[r], mapa(bar, own));
         }
       });
+    }
+    if constexpr (DEFER) {
+      if (it > 0) defer_finish(panel - ncl, it - 1);   // previous panel: pushes landed long ago
+      else cl_arrive();                            // (the second receive buffer is free)
+      continue;
     }
     mbar_wait_cta(rfull, (uint32_t)(it & 1));      // all C partial transforms of our block landed
     if (t == 0) mbar_expect_tx(rfull, Cf::STAGE_BYTES);   // re-arm for the next panel
@@ -838,6 +890,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   }
 
   if (it > 0) cl_wait();                           // pairs with the last arrive
+  if constexpr (DEFER) {
+    if (it > 0) defer_finish(cid + (it - 1) * ncl, it - 1);   // the last panel (its arrive is unpaired:
+    if (it > 0) cl_wait();                                     //  pair it before leaving)
+  }
   if constexpr (Ops::RED) {
     float v = racc;
 #pragma unroll
