@@ -2,6 +2,7 @@
 // thread-block clusters + DSMEM for long columns.  Instantiated per log2(n_az) in az_*.cu.
 #pragma once
 #include <cuda.h>
+#include <cstdlib>
 #include "device_ops.cuh"
 #include "cluster.cuh"
 
@@ -955,19 +956,24 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
     if (e != cudaSuccess) return e;
   }
   const int npan = n_rg / Cf::W;
+  // cluster scheduling: load balancing (measured: 15 instead of 14 co-resident 16-CTA clusters
+  // for the c3 residual sweep, 0.84 -> 0.78 ms); CSSAR_AZ_POLICY overrides (0 = driver default)
+  static const int policy = [] { const char* e = std::getenv("CSSAR_AZ_POLICY"); return e ? std::atoi(e) : 2; }();
   const int ncl = npan < max_cl ? npan : max_cl;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * Cf::C));
   cfg.blockDim = dim3(Cf::T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = Cf::C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+  attr[1].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)policy;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = policy ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, k, a, tm, tmy);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
