@@ -114,7 +114,7 @@ struct TailCtx {
 // loads are in flight together (long-scoreboard latency overlaps)
 struct Aux {
   float2 v;        // Y (RESID) or b_{i-1} (TAIL)
-  uint32_t m;      // mask bit
+  uint32_t m;      // mask word of the element (mask_at(m, col) is its bit)
 };
 
 // destination of output line `row`, column `col` (plain array or a rank's blocked row slab)
@@ -142,12 +142,12 @@ struct AzOps {
   }
 
   CSSAR_DEV static Aux fetch(const AzArgs& a, int row, int col, size_t idx) {
-    Aux x{make_float2(0.f, 0.f), 1u};
+    Aux x{make_float2(0.f, 0.f), 0xFFFFFFFFu};
     if constexpr (MODE == AZ_RESID) {
-      x.m = mask_bit(a.mask, a.mask_words, row, col);
+      x.m = mask_word(a.mask, a.mask_words, row, col);
       x.v = __ldg(a.Y + idx);
     } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
-      x.m = mask_bit(a.mask, a.mask_words, row, col);
+      x.m = mask_word(a.mask, a.mask_words, row, col);
     } else if constexpr (MODE == AZ_TAIL || MODE == AZ_GRAD) {
       x.v = a.b[idx];
     }
@@ -156,16 +156,16 @@ struct AzOps {
 
   // two adjacent columns (col even): one 16-byte load of b, one mask word
   CSSAR_DEV static void fetch2(const AzArgs& a, int row, int col, size_t idx, Aux& x0, Aux& x1) {
-    x0 = Aux{make_float2(0.f, 0.f), 1u};
+    x0 = Aux{make_float2(0.f, 0.f), 0xFFFFFFFFu};
     x1 = x0;
     if constexpr (MODE == AZ_TAIL) {
       const float4 q = *reinterpret_cast<const float4*>(a.b + idx);
       x0.v = make_float2(q.x, q.y);
       x1.v = make_float2(q.z, q.w);
     } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_RESID || MODE == AZ_NORM) {
-      const uint32_t wd = a.mask ? __ldg(a.mask + (size_t)row * a.mask_words + (col >> 5)) : 0xFFFFFFFFu;
-      x0.m = (wd >> (col & 31)) & 1u;
-      x1.m = (wd >> ((col + 1) & 31)) & 1u;
+      const uint32_t wd = mask_word(a.mask, a.mask_words, row, col);
+      x0.m = wd;
+      x1.m = wd;
       if constexpr (MODE == AZ_RESID) {
         const float4 q = __ldg(reinterpret_cast<const float4*>(a.Y + idx));
         x0.v = make_float2(q.x, q.y);
@@ -184,9 +184,9 @@ struct AzOps {
       acc = fmaf(z.x, z.x, fmaf(z.y, z.y, acc));
       return z;
     } else {
-      (void)row; (void)col; (void)s2;
+      (void)row; (void)s2;
       const float2 g = x * a.scale;
-      const float2 r = ax.m ? (ax.v - g) : make_float2(0.f, 0.f);
+      const float2 r = mask_at(ax.m, col) ? (ax.v - g) : make_float2(0.f, 0.f);
       acc = fmaf(r.x, r.x, fmaf(r.y, r.y, acc));
       return r;
     }
@@ -199,8 +199,8 @@ struct AzOps {
     const float sc = DIR < 0 ? a.oscale : a.scale;
     float2 v0 = x0 * sc, v1 = x1 * sc;
     if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
-      if (!a0.m) v0 = make_float2(0.f, 0.f);
-      if (!a1.m) v1 = make_float2(0.f, 0.f);
+      if (!mask_at(a0.m, col)) v0 = make_float2(0.f, 0.f);
+      if (!mask_at(a1.m, col + 1)) v1 = make_float2(0.f, 0.f);
     }
     if constexpr (MODE == AZ_NORM) {
       acc = fmaf(v0.x, v0.x, fmaf(v0.y, v0.y, acc));
@@ -243,7 +243,7 @@ struct AzOps {
     const size_t idx = (size_t)row * a.n_rg + col;
     float2 v = x * (DIR < 0 ? a.oscale : a.scale);        // forward outputs feed a range sweep
     if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
-      if (!ax.m) v = make_float2(0.f, 0.f);
+      if (!mask_at(ax.m, col)) v = make_float2(0.f, 0.f);
     }
     if constexpr (MODE == AZ_NORM) {
       acc = fmaf(v.x, v.x, fmaf(v.y, v.y, acc));
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           for (int p = 0; p < PT; ++p) {
             const int w = slot_w(p), k = slot_k(p);
 #pragma unroll
-            for (int q = 0; q < C; ++q) ax[p][q].m = mask_bit(a.mask, a.mask_words, k + M * q, col0 + w);
+            for (int q = 0; q < C; ++q) ax[p][q].m = mask_word(a.mask, a.mask_words, k + M * q, col0 + w);
           }
         }
       } else {

@@ -67,6 +67,13 @@ CSSAR_DEV uint32_t mask_bit(const uint32_t* mask, int words, int row, int col) {
   return (__ldg(mask + (size_t)row * words + (col >> 5)) >> (col & 31)) & 1u;
 }
 
+// the mask word holding (row, col) (all ones without a mask): loaded early, the bit is taken
+// at its use (mask_at) so the load latency overlaps the transform in between
+CSSAR_DEV uint32_t mask_word(const uint32_t* mask, int words, int row, int col) {
+  return mask ? __ldg(mask + (size_t)row * words + (col >> 5)) : 0xFFFFFFFFu;
+}
+CSSAR_DEV bool mask_at(uint32_t word, int col) { return (word >> (col & 31)) & 1u; }
+
 // x[r] *= exp(+-2 pi i P(u0 + r S)), r < R, by u64 second differences: the first difference
 // d1 is carried exactly in 64 bits, the phase itself only in its top 32 bits (the SFU path
 // uses no more); dropping the low-word carries costs < R * 2^-32 cycle (< 5e-8 rad at R = 32).
