@@ -9,7 +9,8 @@
 
 namespace cssar {
 
-cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int N, int C, int W, int BM) {
+// promo: L2 promotion of the loads (CUtensorMapL2promotion; < 0 = the default, 256 B)
+cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int N, int C, int W, int BM, int promo) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -26,11 +27,7 @@ cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int 
   const cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-#if defined(CSSAR_TMA_PROMO)
-                   (CUtensorMapL2promotion)CSSAR_TMA_PROMO,
-#else
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-#endif
+                   promo >= 0 ? (CUtensorMapL2promotion)promo : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
