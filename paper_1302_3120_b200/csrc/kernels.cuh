@@ -110,6 +110,8 @@ struct RgArgs {
   // (0 = 1), and the fused destination slabs are 2^dlog_w gates wide (0 = log_w)
   int row_step;
   int dlog_w;
+  // persistent launch: total rows (the CTAs loop over row blocks); 0 = one block per CTA
+  int nrows;
 };
 
 enum AzMode : int {

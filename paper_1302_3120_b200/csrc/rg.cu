@@ -1,4 +1,5 @@
 // Range sweeps (S2 G body, S4 M body): one or more range lines per CTA.
+#include <cstdlib>
 #include <type_traits>
 #include "device_ops.cuh"
 #include "cluster.cuh"
@@ -132,7 +133,8 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   constexpr int RL = 1 << En::template lr<false>(En::P - 1);
   extern __shared__ float4 smem4[];
   float2* s = reinterpret_cast<float2*>(smem4);
-  const int row0 = blockIdx.x * C::B;
+  int row0 = blockIdx.x * C::B;               // persistent: rows row0, row0 + gridDim B, ...
+  const int nrows = a.nrows ? a.nrows : (int)gridDim.x * C::B;
   float2* tab = s + N * C::B;                 // exp(2 pi i h / 256) for the phase generator
   const float2* tw = tab + 256;               // inter-pass twiddles
   const int t = threadIdx.x;
@@ -197,12 +199,13 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
       return (size_t)rr * N + j;
     }
   };
+  for (; row0 < nrows; row0 += (int)gridDim.x * C::B) {
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // raw row loads
 #pragma unroll
     for (int r = 0; r < R0; ++r) x[r] = data[at(row0 + b, j + r * (N / R0))];
   });
   cp_async_wait_all();
-  __syncthreads();                                                        // tables visible
+  __syncthreads();                            // tables visible; the previous rows' SMEM reads done
   if constexpr (!RDA) {
     En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // prologue phase
       const Quad q = a.coef[grow(row0 + b)].q[GBODY ? 2 : 0];
@@ -274,6 +277,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
 #pragma unroll
     for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });
+  }
 }
 
 template <int LOGN>
@@ -316,7 +320,22 @@ static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
   auto k = a.rcmc ? rg_sweep_kernel<LOGN, GB, BLK, true> : rg_sweep_kernel<LOGN, GB, BLK, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
-  k<<<n_rows / C::B, C::T, C::SMEM, s>>>(a);
+  // one row block per CTA (measured faster than a persistent grid of co-resident CTAs looping
+  // over the rows: 0.396 vs 0.436 ms at c3); CSSAR_RG_PERSIST=1 selects the persistent grid
+  static const bool persist = [] { const char* v = std::getenv("CSSAR_RG_PERSIST"); return v && std::atoi(v); }();
+  int grid = n_rows / C::B;
+  RgArgs b = a;
+  if (persist) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::T, C::SMEM) == cudaSuccess && per_sm > 0 &&
+        per_sm * sms < grid) {
+      grid = per_sm * sms;
+      b.nrows = n_rows;
+    }
+  }
+  k<<<grid, C::T, C::SMEM, s>>>(b);
   return cudaGetLastError();
 }
 
