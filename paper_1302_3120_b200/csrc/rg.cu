@@ -139,6 +139,12 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   const float2* tw = tab + 256;               // inter-pass twiddles
   const int t = threadIdx.x;
   copy_table_async(tab, a.tab, C::TAB, t, C::T);
+  // fused-transpose destinations in SMEM: a dynamically indexed kernel-parameter array would
+  // be copied to local memory (the multi-GPU variants spilled 300+ bytes per thread)
+  __shared__ float2* sdst[16];
+  if constexpr (BLK) {
+    if (t < 16) sdst[t] = a.dst[t];
+  }
   float2* __restrict__ data = a.data;
   constexpr int LR0 = En::template lr<false>(0), LRL = En::template lr<false>(En::P - 1);
 
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
 #pragma unroll
         for (int r = 0; r < R0; ++r) {
           const int jj = j + r * (N / R0);
-          a.dst[jj >> dlw][rowoff + (size_t)(jj & wm)] = x[r];
+          sdst[jj >> dlw][rowoff + (size_t)(jj & wm)] = x[r];
         }
         return;
       }
