@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--peer-transpose", action="store_true",
+                    help="N > 1: fused peer-memory transposes and the sparse-X' sweep (not yet validated on >1 GPU)")
     return ap.parse_args()
 
 
@@ -207,8 +209,11 @@ def main():
     Y, mb, mask, sc = make_problem_gpu(cfg, plan)
     X = torch.zeros_like(Y)
     kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
-    if world > 1:
-        kw["sparse"] = True           # sparse-X' schedule where it applies (CSSAR_FLAG_SPARSE_X)
+    if world > 1 and args.peer_transpose:
+        # fused peer-memory transposes + sparse-X' first sweep (CSSAR_FLAG_PEER_TRANSPOSE |
+        # CSSAR_FLAG_SPARSE_X); default: NCCL all-to-all transposes (validated path)
+        kw["peer"] = True
+        kw["sparse"] = True
     if world > 1:
         # strong scaling: ONE scene slab-partitioned by azimuth lines; NCCL
         # all-to-all transposes inside libcssar, communicator from a broadcast unique id
@@ -232,9 +237,10 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
-    plan.ita_iterate(Y, mb, X=X, iters=args.steps, **kw)
+    plan.ita_iterate(Y, mb, X=X, iters=args.steps, check=False, **kw)
     e1.record(stream)
     torch.cuda.synchronize()
+    plan.status()                              # non-finite iterate -> CssarError
     ms = e0.elapsed_time(e1)
     clocks = sampler.stop()
     if world > 1:

@@ -84,7 +84,8 @@ typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 
 /* flags: CSSAR_FLAG_PROFILE_STAGES launches the iteration body directly (no graph) with CUDA
  * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
  * accumulates per-step device time (read with cssar_stage_times). */
-enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPARSE_X = 4 };
+enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPARSE_X = 4,
+       CSSAR_FLAG_PEER_TRANSPOSE = 8 };
 
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
  * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule.
@@ -98,8 +99,14 @@ enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPA
  * array (the kept X_i); per iteration one more elementwise pass (X_(i+1) vs X_i, 24 B/sample)
  * and a host synchronisation on `stream`.  The number of updates performed is read with
  * cssar_ita_iters_done; log entries exist only for those.
+ * CSSAR_FLAG_PEER_TRANSPOSE (world > 1; a request): the fused transposes -- sweep epilogues
+ * store straight into the peers' slabs through the CUDA-IPC mappings made at bind time, a
+ * device flag barrier (system-scope release/acquire on slots in every rank's workspace, 20 s
+ * timeout -> CSSAR_ERR_NCCL) orders the sweeps.  Without it (the default until a multi-GPU
+ * run has validated peer stores) the transposes are NCCL all-to-alls.  Ignored if the peers
+ * could not be mapped.
  * CSSAR_FLAG_SPARSE_X (world > 1; a request): the sparse-X' schedule where
- * it applies — k-rule, peer-memory transposes, k <= n_az n_rg / (8 world),
+ * it applies — k-rule, peer-memory transposes (CSSAR_FLAG_PEER_TRANSPOSE), k <= n_az n_rg / (8 world),
  * n_az / world >= 128; otherwise the dense schedule runs.  From iteration 1 on, S1 and its
  * transpose are replaced by a compacted X = E(b) (<= k entries of 16 B) that every rank
  * pulls from every other rank's workspace, folds into n_az/world Doppler bins (cyclic
@@ -118,13 +125,19 @@ typedef struct {
 } cssar_ita_params;
 
 /* Per-iteration log (SPEC "SolverReport"): sigma_i = lambda_i mu_i, lambda_i,
- * support = #{|b_i| > sigma_i} (= #nonzeros of X_(i+1)), resid2 = ||Theta(Y - G X_i)||^2, mu_i. */
+ * support = #{|b_i| > sigma_i} (= #nonzeros of X_(i+1)), resid2 = ||Theta(Y - G X_i)||^2, mu_i,
+ * and the near-tie gap g_i = (|b_i|_(k) - |b_i|_(k+1)) / |b_i|_(k+1) of the k-rule (SURVEY.md
+ * 8(c).3 / 8(c).6 diagnostic; lambda rule P:L314-320): gap_exact = 1 when g_i is exact, 0 when
+ * it is a lower bound (|b_i|_(k) lies above the select's candidate window), the fixed-lambda
+ * rule (no order statistic: gap 0) or world > 1. */
 typedef struct {
   float sigma;
   float lambda;
   int64_t support;
   double resid2;
   float mu;         /* step of the iteration (the fixed mu, or mu_i of the adaptive rule) */
+  float gap;        /* g_i (exact or lower bound, see gap_exact) */
+  int32_t gap_exact;
 } cssar_iter_log;
 
 typedef struct cssar_plan_s* cssar_plan;
@@ -206,6 +219,11 @@ int cssar_plan_set_pulse(cssar_plan plan, const void* pulse_host, int64_t len);
  * the tolerance stop fired). */
 int cssar_ita_iters_done(cssar_plan plan, int32_t* iters_out);
 
+/* Outcome of the last cssar_ita_iterate on this plan: waits (host) for that call's work on its
+ * stream and returns CSSAR_ERR_NONFINITE if a NaN/Inf entered the iterate, else
+ * CSSAR_OK.  cssar_ita_iterate itself reports it only when it synchronises for log_host. */
+int cssar_ita_status(cssar_plan plan);
+
 /* mask_u8 (device, rows*cols bytes, nonzero = sampled) -> bit-packed mask (rows*cols/32
  * words); cols must be a multiple of 32. */
 int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, int64_t cols, void* stream);
@@ -251,6 +269,21 @@ int cssar_stage_times(cssar_plan plan, double* ms_out, int32_t* iters_out);
 
 /* Number of full-histogram fallbacks taken by the last cssar_ita_iterate (synchronous). */
 int cssar_debug_fallbacks(cssar_plan plan, int32_t* out, void* stream);
+
+/* Multi-GPU plumbing hooks (tests).  cssar_debug_ipc_export writes an 80-byte
+ * record {cudaIpcMemHandle_t of the allocation holding dev_ptr, byte offset of dev_ptr in it,
+ * pad} -- the same record cssar_bind_workspace all-gathers; cssar_debug_ipc_open maps a peer
+ * process's record (base_out = the mapping to pass to cssar_debug_ipc_close, ptr_out = the
+ * peer's dev_ptr in this process).  cssar_debug_peer_store writes dst[i] = pattern ^ i for
+ * i < n_words (then a system-scope fence), asynchronously on `stream`.
+ * cssar_group_debug_barrier runs `rounds` flag-barrier rounds of every rank of an emulation
+ * group in one cooperative launch (one block per rank: co-resident, so spinning is legal on
+ * one GPU); CSSAR_ERR_NCCL on a timeout or a wrong final epoch.  Synchronous. */
+int cssar_debug_ipc_export(const void* dev_ptr, void* rec_out);
+int cssar_debug_ipc_open(const void* rec, void** base_out, void** ptr_out);
+int cssar_debug_ipc_close(void* base);
+int cssar_debug_peer_store(void* dst, uint32_t pattern, int64_t n_words, void* stream);
+int cssar_group_debug_barrier(cssar_group group, int32_t rounds, void* stream);
 
 #ifdef __cplusplus
 }

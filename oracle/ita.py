@@ -97,9 +97,12 @@ def half_sigma_from_lm(lm):
 
 
 def kth_largest_mag(b, k):
-    """|b|_(k): the k-th largest magnitude, 1-indexed."""
-    a = np.sort(np.abs(np.asarray(b)).reshape(-1))[::-1]
-    return a[k - 1]
+    """|b|_(k): the k-th largest magnitude, 1-indexed.  The order statistic is taken
+    with a library selection (np.partition puts exactly the value a full descending sort
+    would put at position k - 1 there; ties and zeros included)."""
+    a = np.abs(np.asarray(b)).reshape(-1)
+    n = a.size
+    return np.partition(a, n - k)[n - k]
 
 
 def sigma_k_rule(b, k):

@@ -102,6 +102,12 @@ struct cssar_plan_s {
   bool sparse_used = false;         // the last cssar_ita_iterate ran the sparse-X' schedule
   void* ipc_base[16] = {};          // IPC mappings opened by this rank (closed on rebind/destroy)
   uint32_t* d_bar = nullptr;        // 1-word all-reduce used as the inter-sweep barrier (NCCL)
+  double* d_red = nullptr;          // deterministic norm reductions: [3][kRedSlots] partials + tickets
+  // non-finite report of the last solve without a log: the flag word copied to pinned host
+  // memory at the end of the call, read by cssar_ita_status after its event
+  uint32_t* h_nonfinite = nullptr;
+  cudaEvent_t ev_solve = nullptr;
+  bool solve_pending = false;
 };
 
 namespace {
@@ -229,6 +235,7 @@ int validate_params(const cssar_sar_params& p) {
 
 constexpr int kTransportNone = 0, kTransportNccl = 1, kTransportGroup = 2;
 constexpr size_t kSxHeader = 256;               // sparse-X' list header (entry count) in the workspace
+constexpr size_t kBarSlotOff = 64;              // flag-barrier slots [16] u32 inside that header
 
 // NCCL entry points resolved at run time from the process's libnccl.so.2 (the one torch
 // loaded, or CSSAR_NCCL_LIB); the single-GPU path never touches NCCL.
@@ -356,6 +363,8 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.cand_cap = pl->cand_cap;
   a.Y = (const float2*)Y;
   a.mask = mask;
+  a.red_part = pl->d_red;
+  a.red_ticket = reinterpret_cast<uint32_t*>(pl->d_red + 3 * kRedSlots);
   float2* b = (float2*)X;
   RgArgs r{pl->U, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
@@ -404,6 +413,17 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   MARK(6);
 #undef MARK
   return CSSAR_OK;
+}
+
+// end of a solve: the device's non-finite flag -> pinned host word, event for cssar_ita_status
+cudaError_t note_solve_end(cssar_plan pl, cudaStream_t s) {
+  static_assert(offsetof(SelState, sync_error) == offsetof(SelState, nonfinite) + 4, "flag words adjacent");
+  cudaError_t e = cudaMemcpyAsync(pl->h_nonfinite, reinterpret_cast<char*>(pl->d_st) + offsetof(SelState, nonfinite),
+                                  2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(pl->ev_solve, s);
+  pl->solve_pending = e == cudaSuccess;
+  return e;
 }
 
 double fixed_sigma(const cssar_ita_params& prm) {
@@ -463,6 +483,37 @@ int xchg_allreduce(const Ranks& R, void* const* bufs, int dtype, size_t count, c
   return CSSAR_OK;
 }
 
+// two in-place sums in one NCCL group (one fused collective launch)
+int xchg_allreduce2(const Ranks& R, void* const* a, int ta, size_t na, void* const* b, int tb, size_t nb,
+                    cudaStream_t s) {
+  if (R.group()) {
+    CUDA_TRY(launch_group_sum(ta, a, R.pl[0]->world, (long long)na, s));
+    CUDA_TRY(launch_group_sum(tb, b, R.pl[0]->world, (long long)nb, s));
+    return CSSAR_OK;
+  }
+  auto ty = [](int t) { return t == 0 ? ncclUint32 : t == 1 ? ncclUint64 : ncclFloat64; };
+  NcclApi& n = nccl();
+  NCCL_TRY(n.groupStart());
+  NCCL_TRY(n.allReduce(a[0], a[0], na, ty(ta), ncclSum, R.pl[0]->comm, s));
+  NCCL_TRY(n.allReduce(b[0], b[0], nb, ty(tb), ncclSum, R.pl[0]->comm, s));
+  NCCL_TRY(n.groupEnd());
+  return CSSAR_OK;
+}
+
+// every rank's barrier slot array (16 u32 in the sparse-list header of its workspace)
+PeerSlots peer_slots(cssar_plan pl) {
+  PeerSlots ps{};
+  for (int q = 0; q < pl->world; ++q)
+    ps.slots[q] = pl->peerL[q] ? reinterpret_cast<uint32_t*>(pl->peerL[q] + kBarSlotOff) : nullptr;
+  return ps;
+}
+
+// peer-store transposes run when the peers are mapped and, on real NCCL ranks, only on request
+// (CSSAR_FLAG_PEER_TRANSPOSE); the single-device emulation group uses them by default
+bool fused_active(const Ranks& R, const cssar_ita_params& prm) {
+  return R.pl[0]->fused && (R.group() || (prm.flags & CSSAR_FLAG_PEER_TRANSPOSE));
+}
+
 template <class F>
 void gather_ptrs(const Ranks& R, void** out, F f) {
   for (int i = 0; i < R.np; ++i) out[i] = (void*)f(R.pl[i]);
@@ -485,6 +536,8 @@ AzArgs az_col_args(cssar_plan pl, const cssar_ita_params& prm) {
   a.Y = pl->Ycol;
   a.mask = pl->have_mask ? pl->mcol : nullptr;
   a.b = pl->bcol;
+  a.red_part = pl->d_red;
+  a.red_ticket = reinterpret_cast<uint32_t*>(pl->d_red + 3 * kRedSlots);
   return a;
 }
 
@@ -504,7 +557,7 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
   void *U[16], *V[16], *B[16];
   gather_ptrs(R, U, [](cssar_plan q) { return q->Ucol; });
   gather_ptrs(R, V, [](cssar_plan q) { return q->Vrow; });
-  const bool fused = p0->fused;
+  const bool fused = fused_active(R, prm);
   auto az = [&](int mode) -> int {
     for (int i = 0; i < R.np; ++i) {
       cssar_plan pl = R.pl[i];
@@ -537,8 +590,11 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
   // after a fused sweep: every rank's peer stores into us are complete (NCCL: a one-word
   // all-reduce orders the ranks' streams; the emulation group is serialised on one stream)
   auto barrier = [&]() -> int {
-    if (R.group()) return CSSAR_OK;
-    NCCL_TRY(nccl().allReduce(p0->d_bar, p0->d_bar, 1, ncclUint32, ncclSum, p0->comm, s));
+    if (R.group()) return CSSAR_OK;            // one stream: already ordered
+    CUDA_TRY(launch_flag_barrier(p0->rank, p0->world, peer_slots(p0), p0->d_bar + 1,
+                                 reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(p0->d_st) +
+                                                             offsetof(SelState, sync_error)),
+                                 s));
     return CSSAR_OK;
   };
   auto local_sel = [&](int part) -> int {
@@ -620,11 +676,12 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
     STEP(xchg_a2a(R, V, U, blk, s));
   }
   STEP(az(AZ_TAIL));                          // S5: local histogram / candidates / support
+  void* H[16];
   gather_ptrs(R, B, [](cssar_plan q) { return reinterpret_cast<char*>(q->d_st) + offsetof(SelState, resid2); });
-  STEP(xchg_allreduce(R, B, 2, 1, s));
+  gather_ptrs(R, H, [](cssar_plan q) { return q->d_hist; });
   if (prm.rule == CSSAR_RULE_KSPARSE) {       // S6: exact (k+1)-th largest over all ranks
-    gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist; });
-    STEP(xchg_allreduce(R, B, 0, HIST_WORDS, s));
+    // ||r||^2 and the |b|^2 histogram (+ flags) in one NCCL group: one collective launch
+    STEP(xchg_allreduce2(R, B, 2, 1, H, 0, HIST_WORDS, s));
     STEP(local_sel(SEL_COARSE));
     STEP(local_sel(SEL_FB_HIST));
     gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist_full; });
@@ -637,10 +694,11 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
     STEP(xchg_allreduce(R, B, 0, 1024, s));
     STEP(local_sel(SEL_FINE1_FIND));
   } else {
-    gather_ptrs(R, B, [](cssar_plan q) {
+    void* S[16];
+    gather_ptrs(R, S, [](cssar_plan q) {
       return reinterpret_cast<char*>(q->d_st) + offsetof(SelState, support_fixed);
     });
-    STEP(xchg_allreduce(R, B, 1, 1, s));
+    STEP(xchg_allreduce2(R, B, 2, 1, S, 1, 1, s));
     for (int i = 0; i < R.np; ++i)
       CUDA_TRY(launch_lambda_step(R.pl[i]->d_st, prm.thr, (float)prm.mu, R.pl[i]->d_log, kLogCap, s));
   }
@@ -806,7 +864,7 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
   if (rc != CSSAR_OK) return rc;
   // sparse-X' (CSSAR_FLAG_SPARSE_X): X_0 is arbitrary, so iteration 0 runs the dense schedule
   // outside the graph; X_i (i >= 1) has at most k nonzeros
-  const bool sparse = (prm.flags & CSSAR_FLAG_SPARSE_X) && prm.rule == CSSAR_RULE_KSPARSE && p0->fused &&
+  const bool sparse = (prm.flags & CSSAR_FLAG_SPARSE_X) && prm.rule == CSSAR_RULE_KSPARSE && fused_active(R, prm) &&
                       p0->d_az_tab_m && (uint64_t)prm.k <= (uint64_t)p0->sx_cap;
   p0->sparse_used = sparse;
   int first = 0;
@@ -817,7 +875,8 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
   }
   if (prm.iters > first) {
     GraphKey key{nullptr, (const void*)(uintptr_t)p0->have_mask, nullptr, prm.thr, prm.rule,
-                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu, sparse ? CSSAR_FLAG_SPARSE_X : 0};
+                 prm.rule == CSSAR_RULE_KSPARSE ? prm.k : 0, prm.lambda, prm.mu,
+                 (sparse ? CSSAR_FLAG_SPARSE_X : 0) | (fused_active(R, prm) ? CSSAR_FLAG_PEER_TRANSPOSE : 0)};
     if (!*ghave || !(*gkey == key)) {
       if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
       *ghave = false;
@@ -837,6 +896,7 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
   }
   rc = final_multi(R, prm, X, s);
   if (rc != CSSAR_OK) return rc;
+  for (int i = 0; i < R.np; ++i) CUDA_TRY(note_solve_end(R.pl[i], s));
   if (log_host) {
     std::vector<IterLogDev> tmp((size_t)prm.iters);
     SelState st;
@@ -850,7 +910,10 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
       log_host[i].support = tmp[i].support;
       log_host[i].resid2 = tmp[i].resid2;
       log_host[i].mu = tmp[i].mu;
+      log_host[i].gap = tmp[i].gap;
+      log_host[i].gap_exact = tmp[i].gap_exact;
     }
+    if (st.sync_error) return CSSAR_ERR_NCCL;
     if (st.nonfinite) return CSSAR_ERR_NONFINITE;
   }
   return CSSAR_OK;
@@ -896,36 +959,23 @@ void close_peers(cssar_plan pl) {
 int map_peers_nccl(cssar_plan pl) {
   close_peers(pl);
   if (std::getenv("CSSAR_MULTI_A2A")) return CSSAR_OK;
-  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
-  if (!range) {
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&range), cudaEnableDefault, &q) !=
-            cudaSuccess || q != cudaDriverEntryPointSuccess)
-      range = nullptr;
-  }
-  struct Rec { cudaIpcMemHandle_t h; unsigned long long off; unsigned long long pad; };
-  static_assert(sizeof(Rec) % 16 == 0, "record size");
-  Rec mine{};
-  bool ok = range != nullptr;
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  if (ok) ok = range(&base, &size, (CUdeviceptr)pl->ws) == CUDA_SUCCESS;
-  if (ok) ok = cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
-  mine.off = ok ? (unsigned long long)((CUdeviceptr)pl->ws - base) : ~0ull;
-  // every rank takes part in the all-gather even if its own mapping failed
-  Rec* d = nullptr;
-  std::vector<Rec> all((size_t)pl->world);
-  CUDA_TRY(cudaMalloc(&d, sizeof(Rec) * (size_t)(pl->world + 1)));
+  static_assert(sizeof(IpcRec) % 16 == 0, "record size");
+  IpcRec mine{};
+  ipc_export(pl->ws, &mine);                     // off = ~0 marks a failed export
+  // every rank takes part in the all-gather even if its own export failed
+  IpcRec* d = nullptr;
+  std::vector<IpcRec> all((size_t)pl->world);
+  CUDA_TRY(cudaMalloc(&d, sizeof(IpcRec) * (size_t)(pl->world + 1)));
   int rc = CSSAR_OK;
-  if (cudaMemcpy(d + pl->world, &mine, sizeof(Rec), cudaMemcpyHostToDevice) != cudaSuccess ||
-      nccl().allGather(d + pl->world, d, sizeof(Rec), ncclUint8, pl->comm, pl->cap_stream) != ncclSuccess ||
+  if (cudaMemcpy(d + pl->world, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice) != cudaSuccess ||
+      nccl().allGather(d + pl->world, d, sizeof(IpcRec), ncclUint8, pl->comm, pl->cap_stream) != ncclSuccess ||
       cudaStreamSynchronize(pl->cap_stream) != cudaSuccess ||
-      cudaMemcpy(all.data(), d, sizeof(Rec) * (size_t)pl->world, cudaMemcpyDeviceToHost) != cudaSuccess)
+      cudaMemcpy(all.data(), d, sizeof(IpcRec) * (size_t)pl->world, cudaMemcpyDeviceToHost) != cudaSuccess)
     rc = CSSAR_ERR_NCCL;
   cudaFree(d);
   if (rc != CSSAR_OK) return rc;
   bool every = true;
-  for (const Rec& r : all) every = every && r.off != ~0ull;
+  for (const IpcRec& r : all) every = every && r.off != ~0ull;
   const size_t voff = (size_t)((char*)pl->Vrow - (char*)pl->Ucol);
   for (int q = 0; q < pl->world && every; ++q) {
     if (q == pl->rank) {
@@ -934,16 +984,21 @@ int map_peers_nccl(cssar_plan pl) {
       pl->peerL[q] = pl->sxl;
       continue;
     }
-    void* pb = nullptr;
-    if (cudaIpcOpenMemHandle(&pb, all[(size_t)q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    void *pb = nullptr, *pp = nullptr;
+    if (ipc_open(all[(size_t)q], &pb, &pp) != 0) {
       every = false;
       break;
     }
     pl->ipc_base[q] = pb;
-    pl->peerU[q] = reinterpret_cast<float2*>(static_cast<char*>(pb) + all[(size_t)q].off);
+    pl->peerU[q] = reinterpret_cast<float2*>(pp);
     pl->peerV[q] = reinterpret_cast<float2*>(reinterpret_cast<char*>(pl->peerU[q]) + voff);
     pl->peerL[q] = reinterpret_cast<char*>(pl->peerU[q]) + (pl->sxl - reinterpret_cast<char*>(pl->Ucol));
   }
+  // the flag-barrier slots of this rank and every epoch start at 0 before anyone's first barrier
+  // (the all-reduce below orders the clears across ranks)
+  if (cudaMemset(pl->sxl + kBarSlotOff, 0, 16 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(pl->d_bar, 0, 16) != cudaSuccess)
+    return CSSAR_ERR_CUDA;
   // all ranks must agree on the mode: all-reduce the failure flag
   uint32_t bad = every ? 0u : 1u;
   if (cudaMemcpy(pl->d_bar, &bad, 4, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -1006,6 +1061,8 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
       cudaMalloc(&pl->d_hist, sizeof(uint32_t) * HIST_WORDS) != cudaSuccess ||
       cudaMalloc(&pl->d_hist_full, sizeof(uint32_t) * HIST_BINS) != cudaSuccess ||
       cudaMalloc(&pl->d_lvl, sizeof(uint32_t) * 1024) != cudaSuccess ||
+      cudaMalloc(&pl->d_red, sizeof(double) * (3 * kRedSlots + 8)) != cudaSuccess ||
+      cudaMemset(pl->d_red, 0, sizeof(double) * (3 * kRedSlots + 8)) != cudaSuccess ||
       cudaMalloc(&pl->d_log, sizeof(IterLogDev) * kLogCap) != cudaSuccess ||
       cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&pl->d_rg_tab, sizeof(float2) * rg_table_count(pl->log_nrg)) != cudaSuccess ||
@@ -1023,6 +1080,12 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
+  if (cudaEventCreateWithFlags(&pl->ev_solve, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMallocHost(&pl->h_nonfinite, 2 * sizeof(uint32_t)) != cudaSuccess) {
+    cssar_plan_destroy(pl);
+    return CSSAR_ERR_CUDA;
+  }
+  pl->h_nonfinite[0] = pl->h_nonfinite[1] = 0u;
   if (world > 1 && pl->log_naz - ilog2_exact(world) >= 7 &&
       (cudaMalloc(&pl->d_az_tab_m, sizeof(float2) * (az_table_count(pl->log_naz - ilog2_exact(world), false) + 2)) !=
            cudaSuccess ||
@@ -1125,6 +1188,8 @@ int cssar_plan_destroy(cssar_plan pl) {
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   for (int i = 0; i < 7; ++i)
     if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
+  if (pl->ev_solve) cudaEventDestroy(pl->ev_solve);
+  if (pl->h_nonfinite) cudaFreeHost(pl->h_nonfinite);
   cudaFree(pl->d_coef);
   cudaFree(pl->d_rg_tab);
   cudaFree(pl->d_rcmc);
@@ -1138,6 +1203,7 @@ int cssar_plan_destroy(cssar_plan pl) {
   cudaFree(pl->d_hist);
   cudaFree(pl->d_hist_full);
   cudaFree(pl->d_lvl);
+  cudaFree(pl->d_red);
   cudaFree(pl->d_log);
   delete pl;
   return CSSAR_OK;
@@ -1366,6 +1432,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
     }
   }
   CUDA_TRY(launch_finalize((float2*)X_inout, pl->n, prm->thr, pl->d_st, s));
+  CUDA_TRY(note_solve_end(pl, s));
   if (log_host) {
     const int nl = pl->iters_done;
     std::vector<IterLogDev> tmp((size_t)nl);
@@ -1380,6 +1447,8 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       log_host[i].support = tmp[i].support;
       log_host[i].resid2 = tmp[i].resid2;
       log_host[i].mu = tmp[i].mu;
+      log_host[i].gap = tmp[i].gap;
+      log_host[i].gap_exact = tmp[i].gap_exact;
     }
     if (st.nonfinite) return CSSAR_ERR_NONFINITE;
   }
@@ -1422,6 +1491,14 @@ int cssar_plan_set_pulse(cssar_plan pl, const void* pulse_host, int64_t len) {
   if (!pl->d_hrange) CUDA_TRY(cudaMalloc(&pl->d_hrange, sizeof(float2) * (size_t)N));
   CUDA_TRY(cudaMemcpy(pl->d_hrange, H.data(), sizeof(float2) * (size_t)N, cudaMemcpyHostToDevice));
   return CSSAR_OK;
+}
+
+int cssar_ita_status(cssar_plan pl) {
+  if (!pl) return CSSAR_ERR_BAD_PLAN;
+  if (!pl->solve_pending) return CSSAR_OK;
+  CUDA_TRY(cudaEventSynchronize(pl->ev_solve));
+  if (pl->h_nonfinite[1]) return CSSAR_ERR_NCCL;          // a peer never reached a flag barrier
+  return pl->h_nonfinite[0] ? CSSAR_ERR_NONFINITE : CSSAR_OK;
 }
 
 int cssar_ita_iters_done(cssar_plan pl, int32_t* iters_out) {
@@ -1486,6 +1563,61 @@ int cssar_stage_times(cssar_plan pl, double* ms_out, int32_t* iters_out) {
   if (!pl || !ms_out) return CSSAR_ERR_BAD_PLAN;
   for (int i = 0; i < 6; ++i) ms_out[i] = pl->stage_ms[i];
   if (iters_out) *iters_out = pl->stage_iters;
+  return CSSAR_OK;
+}
+
+int cssar_debug_ipc_export(const void* dev_ptr, void* rec_out) {
+  if (!dev_ptr || !rec_out) return CSSAR_ERR_BAD_PLAN;
+  IpcRec r{};
+  if (ipc_export(dev_ptr, &r) != 0) return CSSAR_ERR_CUDA;
+  std::memcpy(rec_out, &r, sizeof(r));
+  return CSSAR_OK;
+}
+
+int cssar_debug_ipc_open(const void* rec, void** base_out, void** ptr_out) {
+  if (!rec || !base_out || !ptr_out) return CSSAR_ERR_BAD_PLAN;
+  IpcRec r;
+  std::memcpy(&r, rec, sizeof(r));
+  return ipc_open(r, base_out, ptr_out) == 0 ? CSSAR_OK : CSSAR_ERR_CUDA;
+}
+
+int cssar_debug_ipc_close(void* base) {
+  if (!base) return CSSAR_ERR_BAD_PLAN;
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return CSSAR_OK;
+}
+
+int cssar_debug_peer_store(void* dst, uint32_t pattern, int64_t n_words, void* stream) {
+  if (!dst || n_words < 0) return CSSAR_ERR_BAD_PLAN;
+  CUDA_TRY(launch_peer_store(static_cast<uint32_t*>(dst), pattern, (long long)n_words, (cudaStream_t)stream));
+  return CSSAR_OK;
+}
+
+int cssar_group_debug_barrier(cssar_group g, int32_t rounds, void* stream) {
+  if (!g || g->pl.empty() || rounds < 0) return CSSAR_ERR_BAD_PLAN;
+  const int P = (int)g->pl.size();
+  PeerSlots ps{};
+  EpochPtrs ep{};
+  for (int r = 0; r < P; ++r) {
+    cssar_plan pl = g->pl[(size_t)r];
+    if (!pl->sxl) return CSSAR_ERR_WORKSPACE;
+    ps.slots[r] = reinterpret_cast<uint32_t*>(pl->sxl + kBarSlotOff);
+    ep.p[r] = pl->d_bar + 1;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t* err = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(g->pl[0]->d_st) + offsetof(SelState, sync_error));
+  for (int r = 0; r < P; ++r) {
+    cssar_plan pl = g->pl[(size_t)r];
+    CUDA_TRY(cudaMemsetAsync(pl->sxl + kBarSlotOff, 0, 16 * sizeof(uint32_t), s));
+    CUDA_TRY(cudaMemsetAsync(pl->d_bar, 0, 16, s));
+  }
+  CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(uint32_t), s));
+  CUDA_TRY(launch_flag_barrier_group(P, ps, ep, rounds, err, s));
+  uint32_t e = 0, epoch0 = 0;
+  CUDA_TRY(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(&epoch0, g->pl[0]->d_bar + 1, sizeof(epoch0), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (e || epoch0 != (uint32_t)rounds) return CSSAR_ERR_NCCL;
   return CSSAR_OK;
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cstdlib>
+#include <mutex>
 #include "device_ops.cuh"
 #include "cluster.cuh"
 
@@ -123,6 +124,31 @@ CSSAR_DEV float2* out_at(const AzArgs& a, int row, int col) {
   return a.dst[row >> a.dlog_nrow] + ((size_t)((a.drank << a.dlog_nrow) + (row & m))) * (size_t)a.n_rg + col;
 }
 
+// Deterministic squared-norm commit (called by every thread of the CTA after the block
+// reduction; `u` valid in thread 0): the CTA's partial goes to slot blockIdx.x, the last CTA to
+// arrive (ticket) sums the slots in block order -- lane l adds slots l, l+32, ... in order, then
+// a fixed xor-shuffle tree -- and adds the sum to *target (zeroed by the previous select).
+// Run-to-run bitwise reproducible, unlike one floating-point atomicAdd per CTA.
+CSSAR_DEV void red_commit(double* part, uint32_t* ticket, double* target, float u, uint32_t* sflag) {
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = (double)u;
+    __threadfence();
+    *sflag = atomicAdd(ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*sflag && threadIdx.x < 32) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) s += reinterpret_cast<volatile double*>(part)[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      *target += s;
+      *ticket = 0u;
+    }
+  }
+}
+
 template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR) ? -1 : +1;   // first transform direction
@@ -130,6 +156,10 @@ struct AzOps {
   static constexpr bool RED = MODE == AZ_RESID || MODE == AZ_GRAD || MODE == AZ_NORM;
   CSSAR_DEV static double* red_target(const AzArgs& a) {
     return MODE == AZ_RESID ? &a.st->resid2 : MODE == AZ_GRAD ? &a.st->mu_num : &a.st->mu_den;
+  }
+  static constexpr int RED_SLOT = MODE == AZ_RESID ? 0 : MODE == AZ_GRAD ? 1 : 2;
+  CSSAR_DEV static void red_commit_mode(const AzArgs& a, float u, uint32_t* sflag) {
+    red_commit(a.red_part + RED_SLOT * kRedSlots, a.red_ticket + RED_SLOT, red_target(a), u, sflag);
   }
 
   // prologue on a loaded input value (loads are issued for a whole group first)
@@ -357,17 +387,19 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
   if constexpr (Ops::RED) {
     // block reduce the squared norm -> one double atomic per CTA
     __shared__ float red[32];
+    __shared__ uint32_t rflag;
     float v = racc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((t & 31) == 0) red[t >> 5] = v;
     __syncthreads();
+    float u = 0.f;
     if (t < 32) {
-      float u = (t < T / 32) ? red[t] : 0.f;
+      u = (t < T / 32) ? red[t] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-      if (t == 0) atomicAdd(Ops::red_target(a), (double)u);
     }
+    Ops::red_commit_mode(a, u, &rflag);
   }
   if constexpr (MODE == AZ_TAIL) {
     __syncthreads();
@@ -388,6 +420,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
       atomicAdd(&a.st->support_fixed, (unsigned long long)tc.scount[1]);
     }
   }
+  if (a.dst[1]) __threadfence_system();      // multi-GPU fused transpose: peer stores performed
 }
 
 
@@ -902,12 +935,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     __syncthreads();
     if ((t & 31) == 0) reinterpret_cast<float*>(misc)[t >> 5] = v;
     __syncthreads();
+    float u = 0.f;
     if (t < 32) {
-      float u = (t < T / 32) ? reinterpret_cast<float*>(misc)[t] : 0.f;
+      u = (t < T / 32) ? reinterpret_cast<float*>(misc)[t] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-      if (t == 0) atomicAdd(Ops::red_target(a), (double)u);
     }
+    Ops::red_commit_mode(a, u, misc + 33);
   }
   if constexpr (MODE == AZ_TAIL) {
     __syncthreads();
@@ -920,11 +954,14 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       atomicAdd(&a.st->support_fixed, (unsigned long long)tc.scount[1]);
     }
   }
+  if (a.dst[1]) __threadfence_system();      // multi-GPU fused transpose: peer stores performed
 }
 
 // 3-D tensor map {col, rank, m} over a row-major [N][n_rg] complex64 array: element
 // (col, c, m) = row c + C m; box {W, 1, BM}
 cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int N, int C, int W, int BM, int promo);
+constexpr int kMaxDevices = 64;
+std::mutex& az_setup_mutex();
 int az_max_clusters(const void* kernel, int C, int T, size_t smem);
 void az_log_config(int logn, int mode, int C, int W, int NS, int T, size_t smem, int clusters);
 
@@ -933,22 +970,34 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   using Cf = AzClShape<LOGN, MODE>;
   auto k = az_cluster_kernel<LOGN, MODE>;
   const size_t smem = Cf::CL_SMEM;
-  static int max_cl = 0;                 // co-resident clusters (per process; one device)
+  // function attributes and the co-resident cluster count belong to a device context: cached
+  // per device ordinal, set up under a lock (plans on several devices / threads)
+  static int max_cl_dev[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  int max_cl = __atomic_load_n(&max_cl_dev[dev], __ATOMIC_ACQUIRE);
   if (max_cl == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (Cf::C > 8) {
-      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    std::lock_guard<std::mutex> lock(az_setup_mutex());
+    max_cl = max_cl_dev[dev];
+    if (max_cl == 0) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
+      if (Cf::C > 8) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+      }
+      max_cl = az_max_clusters((const void*)k, Cf::C, Cf::T, smem);
+      if (max_cl <= 0) return cudaErrorInvalidConfiguration;
+      az_log_config(LOGN, MODE, Cf::C, Cf::W, Cf::NS, Cf::T, smem, max_cl);
+      __atomic_store_n(&max_cl_dev[dev], max_cl, __ATOMIC_RELEASE);
     }
-    max_cl = az_max_clusters((const void*)k, Cf::C, Cf::T, smem);
-    if (max_cl <= 0) return cudaErrorInvalidConfiguration;
-    az_log_config(LOGN, MODE, Cf::C, Cf::W, Cf::NS, Cf::T, smem, max_cl);
   }
   CUtensorMap tm;
   // the head sweep's panel loads: 64-byte L2 promotion (measured 0.391 -> 0.381 ms at c3; the
   // other sweeps are fastest with the default 256 B)
-  cudaError_t e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM,
+  e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM,
                                      MODE == AZ_FWD_THR ? (int)CU_TENSOR_MAP_L2_PROMOTION_L2_64B : -1);
   if (e != cudaSuccess) return e;
   CUtensorMap tmy = tm;
@@ -1002,6 +1051,7 @@ static cudaError_t az_launch(int n_rg, const AzArgs& a_in, cudaStream_t s) {
     e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
+  if (AzOps<MODE>::RED && (n_rg / Cf::W) * Cf::C > kRedSlots) return cudaErrorInvalidConfiguration;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((n_rg / Cf::W) * Cf::C));
   cfg.blockDim = dim3(Cf::T);

@@ -6,8 +6,14 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 namespace cssar {
+
+std::mutex& az_setup_mutex() {
+  static std::mutex m;
+  return m;
+}
 
 // promo: L2 promotion of the loads (CUtensorMapL2promotion; < 0 = the default, 256 B)
 cudaError_t make_az_tensor_map(CUtensorMap* tm, const void* base, int n_rg, int N, int C, int W, int BM, int promo) {

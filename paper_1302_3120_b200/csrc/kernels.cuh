@@ -40,6 +40,7 @@ struct SelState {
   uint64_t above_count;     // # elements in bins above target_bin
   int32_t iter;             // iteration counter (log index)
   uint32_t nonfinite;
+  uint32_t sync_error;      // multi-GPU flag barrier timed out (a peer never arrived)
   double resid2;            // ||Theta(Y - G X)||^2 of the current iteration
   unsigned long long support_fixed;
   int32_t fallbacks;        // # iterations that needed the full-histogram fallback
@@ -53,7 +54,7 @@ struct SelState {
   float lambda;             // fixed-lambda rule: lambda (adaptive runs recompute sigma = f(lambda mu_i))
 };
 
-struct IterLogDev { float sigma; float lam; long long support; double resid2; float mu; };
+struct IterLogDev { float sigma; float lam; long long support; double resid2; float mu; float gap; int gap_exact; };
 
 struct AzArgs {
   const float2* in;
@@ -82,7 +83,12 @@ struct AzArgs {
   int drank;
   float2* D;                // AZ_GRAD: dense gradient dX (for the elementwise step)
   float lambda;             // fixed-lambda rule with the adaptive step (sigma_i = f(lambda mu_i))
+  // deterministic squared-norm reductions (RESID / GRAD / NORM): per-CTA partials in slot
+  // arrays [3][kRedSlots] reduced in block order by the last CTA (ticket counter per mode)
+  double* red_part;
+  uint32_t* red_ticket;
 };
+constexpr int kRedSlots = 8192;   // >= the grid of every reducing azimuth launch
 
 struct RgArgs {
   float2* data;
@@ -160,6 +166,17 @@ cudaError_t launch_sx_compact(const float2* b, long long n, int log_ncol, int co
                               SxEntry* list, uint32_t* count, uint32_t cap, int sm_count, cudaStream_t s);
 cudaError_t launch_sx_fold(const SxLists& L, int p, int log_n, int m, int n_rg, float2* F, int sm_count,
                            cudaStream_t s);
+// multi-GPU peer plumbing (peer.cu)
+struct PeerSlots { uint32_t* slots[16]; };            // every rank's barrier slot array (peer memory)
+struct EpochPtrs { uint32_t* p[16]; };
+struct IpcRec { cudaIpcMemHandle_t h; unsigned long long off; unsigned long long pad; };
+cudaError_t launch_flag_barrier(int rank, int world, const PeerSlots& ps, uint32_t* epoch, uint32_t* err,
+                                cudaStream_t s);
+cudaError_t launch_flag_barrier_group(int world, const PeerSlots& ps, const EpochPtrs& ep, int rounds, uint32_t* err,
+                                      cudaStream_t s);
+int ipc_export(const void* p, IpcRec* rec);
+int ipc_open(const IpcRec& rec, void** base_out, void** ptr_out);
+cudaError_t launch_peer_store(uint32_t* dst, uint32_t pattern, long long n, cudaStream_t s);
 // tolerance stop (NEXT-4): per-block (||E(b; sigma) - Xk||^2, ||Xk||^2) into part[blocks], Xk <- E(b; sigma)
 cudaError_t launch_conv_check(const float2* b, float2* Xk, long long n, const SelState* st, int thr, double2* part,
                               int blocks, cudaStream_t s);

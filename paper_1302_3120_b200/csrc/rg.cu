@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });
   }
+  if constexpr (BLK) {
+    if (a.dst[0]) __threadfence_system();   // peer stores performed before the flag barrier
+  }
 }
 
 template <int LOGN>

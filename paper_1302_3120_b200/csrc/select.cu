@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(512) fb_collect_kernel(const float2* __restric
     __syncthreads();
     for (uint32_t e = threadIdx.x; e < cntb; e += blockDim.x) {
       const uint32_t g = base + e;
-      if (g < cap) cand[g] = buf[e]; else st->cand_overflow = 1u;
+      if (g < cap) cand[g] = buf[e]; else st->cand_overflow = 1u;   // -> exact count over b (fine_count)
     }
     __syncthreads();
   }
@@ -217,7 +217,7 @@ CSSAR_DEV float lambda_of_sigma(float sig, float mu, int thr) {
 // sigma^2 found: state for the next iteration (new sigma, histogram floor, candidate window,
 // log entry, counter resets).  Runs in thread 0 (bookkeeping) and all threads (resets).
 CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float mu, SelState* st, uint32_t* hist,
-                             uint32_t* hist_full, IterLogDev* log, int log_cap) {
+                             uint32_t* hist_full, IterLogDev* log, int log_cap, float gap = 0.0f, int gap_exact = 0) {
   const int t = threadIdx.x;
   if (t == 0) {
     const float sig = sqrtf(__uint_as_float(s2));
@@ -232,6 +232,8 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
       e.lam = lambda_of_sigma(sig, m, thr);
       e.support = (long long)abv;
       e.resid2 = st->resid2;
+      e.gap = gap;
+      e.gap_exact = gap_exact;
       log[it] = e;
     }
     const int B = (int)(s2 >> HIST_SHIFT);
@@ -255,35 +257,77 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
   if (t == 0) st->need_full = 0;
 }
 
-// one 10-bit radix level over the candidates: counts of (u >> sh) & 1023 among u with
-// (u >> (sh + 10)) == prefix
-CSSAR_DEV void fine_count(uint32_t* cnt, const uint32_t* cand, uint32_t nc, uint32_t prefix, int sh) {
+// one 10-bit radix level: counts of (u >> sh) & 1023 among the |b|^2 patterns u with
+// (u >> (sh + 10)) == prefix -- over the candidate list, or, when the list overflowed (more
+// than cand_cap patterns in the target bin, e.g. a flat or all-zero b), over all of b (one
+// block scanning the array: the degenerate case stays exact, just slower)
+CSSAR_DEV void fine_count(uint32_t* cnt, const uint32_t* cand, uint32_t nc, uint32_t prefix, int sh,
+                          const float2* b = nullptr, long long n = 0) {
   const int t = threadIdx.x;
   cnt[t] = 0u;
   __syncthreads();
-  for (uint32_t i = t; i < nc; i += 1024) {
-    const uint32_t u = cand[i];
-    if ((u >> (sh + 10)) == prefix) atomicAdd(&cnt[(u >> sh) & 1023u], 1u);
+  if (b) {
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (long long i = t; i < n / 2; i += 1024) {
+      const float4 q = b4[i];
+      const uint32_t u0 = mag2_bits(make_float2(q.x, q.y)), u1 = mag2_bits(make_float2(q.z, q.w));
+      if ((u0 >> (sh + 10)) == prefix) atomicAdd(&cnt[(u0 >> sh) & 1023u], 1u);
+      if ((u1 >> (sh + 10)) == prefix) atomicAdd(&cnt[(u1 >> sh) & 1023u], 1u);
+    }
+  } else {
+    for (uint32_t i = t; i < nc; i += 1024) {
+      const uint32_t u = cand[i];
+      if ((u >> (sh + 10)) == prefix) atomicAdd(&cnt[(u >> sh) & 1023u], 1u);
+    }
   }
   __syncthreads();
+}
+
+// near-tie gap g = (|b|_(k) - |b|_(k+1)) / |b|_(k+1) (SURVEY.md 8(c).3 log, 8(c).6 diagnostic):
+// 0 when ties leave fewer than k values above sigma; else the smallest candidate pattern above
+// sigma^2 is |b|_(k)^2 if the candidate window holds it (exact), otherwise the window's upper
+// bin edge bounds it from below.  Returns the gap; *exact = 0 for a bound.
+CSSAR_DEV float near_tie_gap(uint32_t s2, unsigned long long abv, long long k, const uint32_t* cand, uint32_t nc,
+                             bool have_list, int hi_bin, uint32_t* smin, int* exact) {
+  const int t = threadIdx.x;
+  if (t == 0) *smin = 0xFFFFFFFFu;
+  __syncthreads();
+  if (have_list && (long long)abv >= k) {
+    uint32_t m = 0xFFFFFFFFu;
+    for (uint32_t i = t; i < nc; i += blockDim.x) {
+      const uint32_t u = cand[i];
+      if (u > s2 && u < m) m = u;
+    }
+    atomicMin(smin, m);
+  }
+  __syncthreads();
+  if ((long long)abv < k) { *exact = 1; return 0.0f; }
+  if (s2 == 0u) { *exact = 0; return INFINITY; }
+  const uint32_t um = *smin;
+  const bool ex = have_list && um != 0xFFFFFFFFu;
+  const uint32_t ub = ex ? um : (uint32_t)(hi_bin + 1) << HIST_SHIFT;
+  *exact = ex ? 1 : 0;
+  return (float)(sqrt((double)__uint_as_float(ub) / (double)__uint_as_float(s2)) - 1.0);
 }
 
 // radix refinement inside target_bin over the candidate list (two 10-bit levels: bits
 // [19:10] then [9:0]), then finish_select
 __global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, float mu, SelState* st,
                                                         uint32_t* hist, uint32_t* hist_full, const uint32_t* cand,
-                                                        uint32_t cap, IterLogDev* log, int log_cap) {
+                                                        uint32_t cap, IterLogDev* log, int log_cap, const float2* b,
+                                                        long long n) {
   __shared__ uint32_t cnt[1024], above[1024], wt[32];
   __shared__ int sd;
-  __shared__ uint32_t sr, sa;
+  __shared__ uint32_t sr, sa, smin;
   const int t = threadIdx.x;
+  const bool ovf = st->cand_overflow != 0u;     // list truncated: count over b instead (exact)
   const uint32_t nc = min(st->cand_count, cap);
   uint32_t prefix = (uint32_t)st->target_bin;   // matched high bits so far
   uint32_t rank = st->target_rank;
   unsigned long long abv = st->above_count;
 #pragma unroll 1
   for (int lvl = 0; lvl < 2; ++lvl) {
-    fine_count(cnt, cand, nc, prefix, lvl == 0 ? 10 : 0);
+    fine_count(cnt, cand, nc, prefix, lvl == 0 ? 10 : 0, ovf ? b : nullptr, n);
     if (t == 0) { sd = -1; sr = 0; sa = 0; }
     __syncthreads();
     block_suffix<1024>(cnt, above, wt);
@@ -294,13 +338,14 @@ __global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, fl
     abv += sa;
     __syncthreads();
   }
-  (void)k;
-  finish_select(prefix, abv, thr, mu, st, hist, hist_full, log, log_cap);
+  int gx = 0;
+  const float gap = near_tie_gap(prefix, abv, k, cand, nc, !ovf, st->cand_hi, &smin, &gx);
+  finish_select(prefix, abv, thr, mu, st, hist, hist_full, log, log_cap, gap, gx);
 }
 
 // ---- split fine select (multi-GPU): local level histograms, global counts after the all-reduce
 __global__ void __launch_bounds__(1024) fine_hist_kernel(int lvl, SelState* st, const uint32_t* cand, uint32_t cap,
-                                                         uint32_t* out) {
+                                                         uint32_t* out, const float2* b, long long n) {
   __shared__ uint32_t cnt[1024];
   if (lvl == 0 && threadIdx.x == 0) {
     st->fine_prefix = (uint32_t)st->target_bin;
@@ -309,13 +354,14 @@ __global__ void __launch_bounds__(1024) fine_hist_kernel(int lvl, SelState* st, 
   }
   __syncthreads();
   const uint32_t prefix = lvl == 0 ? (uint32_t)st->target_bin : st->fine_prefix;
-  fine_count(cnt, cand, min(st->cand_count, cap), prefix, lvl == 0 ? 10 : 0);
+  fine_count(cnt, cand, min(st->cand_count, cap), prefix, lvl == 0 ? 10 : 0, st->cand_overflow ? b : nullptr, n);
   out[threadIdx.x] = cnt[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(1024) fine_find_kernel(int lvl, int thr, float mu, SelState* st, uint32_t* hist,
                                                          uint32_t* hist_full, const uint32_t* cand, uint32_t cap,
-                                                         uint32_t* lvl_cnt, IterLogDev* log, int log_cap) {
+                                                         uint32_t* lvl_cnt, IterLogDev* log, int log_cap,
+                                                         const float2* b, long long n) {
   __shared__ uint32_t cnt[1024], above[1024], wt[32];
   __shared__ int sd;
   __shared__ uint32_t sr, sa;
@@ -335,7 +381,7 @@ __global__ void __launch_bounds__(1024) fine_find_kernel(int lvl, int thr, float
       st->fine_abv = abv;
     }
     // level-1 local counts for the next all-reduce
-    fine_count(cnt, cand, min(st->cand_count, cap), prefix, 0);
+    fine_count(cnt, cand, min(st->cand_count, cap), prefix, 0, st->cand_overflow ? b : nullptr, n);
     lvl_cnt[t] = cnt[t];
   } else {
     finish_select(prefix, abv, thr, mu, st, hist, hist_full, log, log_cap);
@@ -352,6 +398,8 @@ __global__ void lambda_step_kernel(SelState* st, int thr, float mu, IterLogDev* 
     e.lam = lambda_of_sigma(st->sigma_fixed, m, thr);
     e.support = (long long)st->support_fixed;
     e.resid2 = st->resid2;
+    e.gap = 0.0f;                                  // no order statistic under a fixed lambda
+    e.gap_exact = 0;
     log[it] = e;
   }
   st->iter = it + 1;
@@ -416,7 +464,7 @@ cudaError_t launch_select(int sm_count, float2* b, long long n, long long k, int
   fb_hist_kernel<<<grid, 512, 0, s>>>(b, n, st, hist_full);
   fb_find_kernel<<<1, 1024, 0, s>>>(k, st, hist_full);
   fb_collect_kernel<<<grid, 512, 0, s>>>(b, n, st, cand, cand_cap);
-  sel_fine_kernel<<<1, 1024, 0, s>>>(k, thr, mu, st, hist, hist_full, cand, cand_cap, log, log_cap);
+  sel_fine_kernel<<<1, 1024, 0, s>>>(k, thr, mu, st, hist, hist_full, cand, cand_cap, log, log_cap, b, n);
   return cudaGetLastError();
 }
 
@@ -431,12 +479,12 @@ cudaError_t launch_select_part(int part, int sm_count, float2* b, long long n, l
       fb_find_kernel<<<1, 1024, 0, s>>>(k, st, hist_full);
       fb_collect_kernel<<<grid, 512, 0, s>>>(b, n, st, cand, cand_cap);
       break;
-    case SEL_FINE0_HIST: fine_hist_kernel<<<1, 1024, 0, s>>>(0, st, cand, cand_cap, lvl); break;
+    case SEL_FINE0_HIST: fine_hist_kernel<<<1, 1024, 0, s>>>(0, st, cand, cand_cap, lvl, b, n); break;
     case SEL_FINE0_FIND:
-      fine_find_kernel<<<1, 1024, 0, s>>>(0, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap);
+      fine_find_kernel<<<1, 1024, 0, s>>>(0, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap, b, n);
       break;
     case SEL_FINE1_FIND:
-      fine_find_kernel<<<1, 1024, 0, s>>>(1, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap);
+      fine_find_kernel<<<1, 1024, 0, s>>>(1, thr, mu, st, hist, hist_full, cand, cand_cap, lvl, log, log_cap, b, n);
       break;
     default: return cudaErrorInvalidValue;
   }

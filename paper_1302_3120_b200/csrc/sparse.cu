@@ -42,9 +42,14 @@ __global__ void __launch_bounds__(256) sx_compact_kernel(const float2* __restric
       }
     }
   }
+  __threadfence_system();     // the list is read by the peers over NVLink after the barrier
 }
 
-__global__ void __launch_bounds__(256) sx_fold_kernel(const SxLists L, int p, int log_n, int m, int n_rg,
+// Fold pass n1: the entries of rows n1 m .. n1 m + m - 1 (each (n2 = row mod m, col) at most
+// once per pass), F[n2][col] += w_N^{p row} X[row][col].  Passes run n1 = 0 .. world-1 in
+// stream order, so every F element sums its <= world terms in a fixed order: run-to-run
+// deterministic, without floating-point atomics.
+__global__ void __launch_bounds__(256) sx_fold_kernel(const SxLists L, int p, int log_n, int m, int n_rg, int n1,
                                                       float2* __restrict__ F) {
   const uint32_t nmask = (1u << log_n) - 1u;
   const float inv_n = 1.0f / (float)(1u << log_n);
@@ -53,14 +58,14 @@ __global__ void __launch_bounds__(256) sx_fold_kernel(const SxLists L, int p, in
     const SxEntry* __restrict__ e = L.list[q];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
       const SxEntry x = e[i];
+      if (x.row / m != n1) continue;
       // w_N^{p n} = exp(-2 pi i (p n mod N) / N), the fraction exact in fp32 (N <= 2^15)
       const uint32_t ph = ((uint32_t)p * (uint32_t)x.row) & nmask;
       float sn, cs;
       sincospif(-2.0f * (float)ph * inv_n, &sn, &cs);
       const float2 v = cmul(x.v, make_float2(cs, sn));
       float2* dst = F + (size_t)(x.row & (m - 1)) * n_rg + x.col;
-      atomicAdd(&dst->x, v.x);
-      atomicAdd(&dst->y, v.y);
+      *dst = *dst + v;
     }
   }
 }
@@ -77,8 +82,12 @@ cudaError_t launch_sx_fold(const SxLists& L, int p, int log_n, int m, int n_rg, 
                            cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(F, 0, sizeof(float2) * (size_t)m * n_rg, s);
   if (e != cudaSuccess) return e;
-  sx_fold_kernel<<<4 * sm_count, 256, 0, s>>>(L, p, log_n, m, n_rg, F);
-  return cudaGetLastError();
+  for (int n1 = 0; n1 < L.world; ++n1) {
+    sx_fold_kernel<<<4 * sm_count, 256, 0, s>>>(L, p, log_n, m, n_rg, n1, F);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace cssar

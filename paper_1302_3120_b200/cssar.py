@@ -29,11 +29,14 @@ SYMBOLS = [
     "cssar_error_string", "cssar_debug_range_sweep", "cssar_debug_az_fft", "cssar_debug_select",
     "cssar_debug_fallbacks", "cssar_stage_times", "cssar_nccl_unique_id", "cssar_group_create",
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
-    "cssar_ita_iters_done", "cssar_plan_set_pulse", "cssar_group_operator",
+    "cssar_ita_iters_done", "cssar_plan_set_pulse", "cssar_group_operator", "cssar_ita_status",
+    "cssar_debug_ipc_export", "cssar_debug_ipc_open", "cssar_debug_ipc_close", "cssar_debug_peer_store",
+    "cssar_group_debug_barrier",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
 CSSAR_FLAG_SPARSE_X = 4
+CSSAR_FLAG_PEER_TRANSPOSE = 8
 STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
 
 
@@ -59,7 +62,8 @@ class ItaParamsC(ctypes.Structure):
 
 class IterLogC(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_float), ("lam", ctypes.c_float), ("support", ctypes.c_int64),
-                ("resid2", ctypes.c_double), ("mu", ctypes.c_float)]
+                ("resid2", ctypes.c_double), ("mu", ctypes.c_float), ("gap", ctypes.c_float),
+                ("gap_exact", ctypes.c_int32)]
 
 
 _lib = None
@@ -96,6 +100,12 @@ def load_library(path=None):
     lib.cssar_group_destroy.argtypes = [P]
     lib.cssar_group_workspace_size.argtypes = [P, ctypes.POINTER(ctypes.c_size_t)]
     lib.cssar_ita_iters_done.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.cssar_ita_status.argtypes = [P]
+    lib.cssar_debug_ipc_export.argtypes = [V, V]
+    lib.cssar_debug_ipc_open.argtypes = [V, ctypes.POINTER(V), ctypes.POINTER(V)]
+    lib.cssar_debug_ipc_close.argtypes = [V]
+    lib.cssar_debug_peer_store.argtypes = [V, ctypes.c_uint32, I64, V]
+    lib.cssar_group_debug_barrier.argtypes = [P, ctypes.c_int32, V]
     lib.cssar_plan_set_pulse.argtypes = [P, V, I64]
     lib.cssar_group_operator.argtypes = [P, I, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(V), V]
     lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
@@ -152,6 +162,32 @@ def nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(lib.cssar_nccl_unique_id(buf), "cssar_nccl_unique_id")
     return buf.raw
+
+
+def ipc_export(t):
+    """80-byte CUDA-IPC record of a device tensor's storage (cssar_debug_ipc_export)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(80)
+    _check(lib.cssar_debug_ipc_export(_ptr(t), buf), "cssar_debug_ipc_export")
+    return bytes(buf.raw)
+
+
+def ipc_open(rec):
+    """Map a peer process's record: returns (base, ptr) device addresses (ints)."""
+    lib = load_library()
+    base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib.cssar_debug_ipc_open(ctypes.create_string_buffer(rec, 80), ctypes.byref(base), ctypes.byref(ptr)),
+           "cssar_debug_ipc_open")
+    return base.value, ptr.value
+
+
+def ipc_close(base):
+    _check(load_library().cssar_debug_ipc_close(ctypes.c_void_p(base)), "cssar_debug_ipc_close")
+
+
+def peer_store(ptr, pattern, n_words, stream=None):
+    _check(load_library().cssar_debug_peer_store(ctypes.c_void_p(ptr), pattern, n_words, _stream(stream)),
+           "cssar_debug_peer_store")
 
 
 def slab_rows(n_az, world, rank):
@@ -242,10 +278,14 @@ class Plan:
         return out
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
-                    log=False, profile_stages=False, stream=None, tol=0.0, sparse=False):
+                    log=False, profile_stages=False, stream=None, tol=0.0, sparse=False, peer=False, check=True):
         """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X.
         mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU).  tol > 0: stop after the
-        first update with ||X_(i+1) - X_i|| <= tol ||X_i|| (self.iters_done = updates performed)."""
+        first update with ||X_(i+1) - X_i|| <= tol ||X_i|| (self.iters_done = updates performed).
+        world > 1: peer=True requests the fused peer-memory transposes (CSSAR_FLAG_PEER_TRANSPOSE),
+        sparse=True additionally the sparse-X' first sweep.
+        check=True waits for the solve and raises CssarError(CSSAR_ERR_NONFINITE) if a NaN/Inf
+        entered the iterate (cssar_ita_status); check=False returns without synchronising."""
         if X is None:
             X = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
         adaptive = isinstance(mu, str)
@@ -255,20 +295,28 @@ class Plan:
                          CSSAR_RULE_KSPARSE if rule == "k" else CSSAR_RULE_FIXED_LAMBDA,
                          int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
                          (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
-                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0) | (CSSAR_FLAG_SPARSE_X if sparse else 0),
+                         (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0) | (CSSAR_FLAG_SPARSE_X if sparse else 0) |
+                         (CSSAR_FLAG_PEER_TRANSPOSE if peer else 0),
                          float(tol))
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),
                                         logbuf if log else None, _stream(stream))
         _check(rc, "cssar_ita_iterate")
+        if check:
+            _check(self.lib.cssar_ita_status(self.h), "cssar_ita_status")
         done = ctypes.c_int32()
         _check(self.lib.cssar_ita_iters_done(self.h, ctypes.byref(done)), "cssar_ita_iters_done")
         self.iters_done = done.value
         if log:
-            entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu)
+            entries = [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu,
+                            gap=e.gap, gap_exact=bool(e.gap_exact))
                        for e in list(logbuf)[:self.iters_done]]
             return X, entries
         return X
+
+    def status(self):
+        """Wait for the last ita_iterate and raise on a non-finite iterate (cssar_ita_status)."""
+        _check(self.lib.cssar_ita_status(self.h), "cssar_ita_status")
 
     def set_pulse(self, pulse=None):
         """RDA plans: recorded transmitted pulse (complex samples at (m - (L-1)/2)/F_r) as the range
@@ -363,6 +411,10 @@ class Group:
         except Exception:
             pass
 
+    def debug_barrier(self, rounds, stream=None):
+        """`rounds` flag-barrier rounds over all ranks in one cooperative launch."""
+        _check(self.lib.cssar_group_debug_barrier(self.h, int(rounds), _stream(stream)), "cssar_group_debug_barrier")
+
     def _operator(self, forward, ins, mask_bits, outs, stream):
         W = self.world
         arr = ctypes.c_void_p * W
@@ -397,6 +449,7 @@ class Group:
         _check(self.lib.cssar_group_ita_iterate(self.h, ys, ms, ctypes.byref(prm), xs, logbuf if log else None,
                                                 _stream(stream)), "cssar_group_ita_iterate")
         if log:
-            return [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu)
+            return [dict(sigma=e.sigma, lam=e.lam, support=int(e.support), resid2=e.resid2, mu=e.mu,
+                         gap=e.gap, gap_exact=bool(e.gap_exact))
                     for e in list(logbuf)[:iters]]
         return None

@@ -35,10 +35,17 @@ def to_host(t):
     return t.detach().cpu().numpy()
 
 
+@functools.lru_cache(maxsize=2)
+def oracle_op(params):
+    """The fp64 CSA operator of a parameter set, cached (its three phase screens are the
+    expensive part at c3/c4 sizes)."""
+    return csa.CSAOperator(params)
+
+
 def oracle_echo(scene, cfg):
     if cfg.echo == "exact":
         return echo.exact_echo(cfg.params, scene.targets)
-    return echo.inverse_csa_echo(csa.CSAOperator(cfg.params), scene.dense())
+    return echo.inverse_csa_echo(oracle_op(cfg.params), scene.dense())
 
 
 @functools.lru_cache(maxsize=8)

@@ -1,0 +1,173 @@
+"""Full-size parity on the two largest BASELINE.json configs, c3 (8192 x 8192) and c4
+(32768 x 16384), in the launch configuration bench.py times (north star:
+operators <= 1e-4 rel-L2, Algorithm 1 output <= 1e-3 rel-L2 on all five configs).
+
+Expected values come only from oracle/ (fp64): computed here, or -- for the c3 trajectory,
+which costs ~100 fp64 iterations -- read from tests/golden/c3_oracle_iterates.npz, written by
+tools/make_c3_oracle_golden.py (calls oracle/ and inputs/ only).
+
+c3: the GPU's full 100-iteration Algorithm 1 run vs the oracle's X_100, all 500
+bright targets in both supports, sigma / support logs every iteration, and teacher-forced
+steps 50 and 99 from the oracle's X_49 / X_98 (complex64) with near-tie pixels excluded.
+c4: cssar_forward / cssar_adjoint vs the oracle's A / A^H, one Algorithm 1 iteration from
+X = 0, and a teacher-forced step from a seeded k-sparse iterate (first oracle check of the
+n_az = 32768 azimuth kernels and of the Doppler rows >= 16384).
+"""
+import functools
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ita
+from tests._common import mask_bits_dev, need_gpu, oracle_op, problem, rel_l2, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+TOL_OP = 1e-4
+TOL_ITA = 1e-3
+NEAR = 1e-5          # near-tie band: |b| within NEAR * sigma of sigma
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "c3_oracle_iterates.npz")
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def _plan(p):
+    from paper_1302_3120_b200 import Plan
+    return Plan(p)
+
+
+def _dense(shape, idx, val):
+    X = np.zeros(int(np.prod(shape)), np.complex64)
+    X[idx] = val
+    return X.reshape(shape)
+
+
+@functools.lru_cache(maxsize=1)
+def _golden():
+    if not os.path.exists(GOLDEN):
+        pytest.skip("tests/golden/c3_oracle_iterates.npz missing (python tools/make_c3_oracle_golden.py)")
+    return dict(np.load(GOLDEN))
+
+
+def _oracle_step(op, Y, mask, X, k):
+    """One Algorithm 1 update from X (fp64): returns (X_next, b, sigma)."""
+    R = mask * (Y - op.G(X))
+    b = X + op.M(R)
+    del R
+    sig = ita.sigma_k_rule(b, k)
+    return ita.soft(b, sig), b, sig
+
+
+def _teacher_forced(prob, op, pl, Xin_c64, k):
+    """GPU and oracle each take one update from the same complex64 iterate; compare X and
+    sigma with pixels in the near-tie band excluded."""
+    Yd, mb = to_dev(prob.Y), mask_bits_dev(prob.mask)
+    Xg, glog = pl.ita_iterate(Yd, mb, thr="soft", rule="k", k=k, iters=1, X=to_dev(Xin_c64), log=True)
+    Xg = to_host(Xg)
+    Xo, b, sig = _oracle_step(op, prob.Y.astype(np.complex128), prob.mask, Xin_c64.astype(np.complex128), k)
+    keep = ~(np.abs(np.abs(b) - sig) <= NEAR * sig)
+    assert abs(glog[0]["sigma"] - sig) / sig <= 1e-5
+    assert glog[0]["support"] <= k
+    err = rel_l2(Xg[keep], Xo[keep])
+    assert err <= TOL_OP, err
+    return Xg, Xo
+
+
+# ------------------------------------------------------------------------------------ c3
+def test_c3_full_run_vs_oracle_trajectory():
+    """c3's full 100 iterations on the GPU vs the oracle's X_100 (rel-L2 <= 1e-3), all 500
+    bright targets (|sigma| = 10) in both supports, sigma and support logs at every iteration."""
+    g = _golden()
+    prob = problem("c3")
+    cfg = prob.cfg
+    assert int(g["k"]) == cfg.k and int(g["iters"]) == cfg.iters == 100
+    pl = _plan(cfg.params)
+    Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr="soft", rule="k", k=cfg.k,
+                              iters=cfg.iters, log=True)
+    Xg = to_host(Xg)
+    Xo = _dense(Xg.shape, g["X100_idx"], g["X100_val"])
+    err = rel_l2(Xg, Xo)
+    assert err <= TOL_ITA, err
+    bright = prob.scene.idx[np.abs(prob.scene.val) >= 9.99]
+    assert bright.size == 500
+    assert np.all(Xg.reshape(-1)[bright] != 0) and np.all(Xo.reshape(-1)[bright] != 0)
+    s_g = np.array([e["sigma"] for e in glog])
+    assert np.max(np.abs(s_g - g["log_sigma"]) / g["log_sigma"]) <= 1e-4
+    sup = np.array([e["support"] for e in glog])
+    assert np.all(sup <= cfg.k)
+    # soft thresholding is continuous: boundary flips move |b| - sigma ~ 0, so the support
+    # counts agree to a tiny fraction of k (8(c).6 clutter configs)
+    assert np.max(np.abs(sup - g["log_support"])) <= 1e-3 * cfg.k
+    r_g = np.array([e["resid2"] for e in glog])
+    assert np.max(np.abs(r_g - g["log_resid2"]) / g["log_resid2"]) <= 1e-4
+
+
+@pytest.mark.parametrize("step", [50, 99])
+def test_c3_teacher_forced_late_step(step):
+    """Teacher-forced step `step`: one update from the oracle's X_(step-1)."""
+    g = _golden()
+    prob = problem("c3")
+    cfg = prob.cfg
+    key = {50: "X49", 99: "X98"}[step]
+    Xin = _dense((cfg.params.n_az, cfg.params.n_rg), g[key + "_idx"], g[key + "_val"])
+    pl = _plan(cfg.params)
+    Xg, Xo = _teacher_forced(prob, oracle_op(cfg.params), pl, Xin, cfg.k)
+    bright = prob.scene.idx[np.abs(prob.scene.val) >= 9.99]
+    assert np.all(Xg.reshape(-1)[bright] != 0) and np.all(Xo.reshape(-1)[bright] != 0)
+
+
+# ------------------------------------------------------------------------------------ c4
+@functools.lru_cache(maxsize=1)
+def _c4():
+    """The c4 recipe (inverse-CSA echo of 0.5% Rayleigh clutter, 50% Bernoulli mask, 20 dB),
+    the oracle operator, and a seeded k-sparse iterate X_in = 0.9 X_true + CN(0, 0.05^2) on
+    supp(X_true) (complex64) standing in for a late iterate."""
+    prob = problem("c4")
+    op = oracle_op(prob.cfg.params)
+    r = np.random.default_rng(13023124)
+    val = 0.9 * prob.scene.val + 0.05 * (r.standard_normal(prob.scene.idx.size)
+                                         + 1j * r.standard_normal(prob.scene.idx.size)) / np.sqrt(2)
+    Xin = _dense((prob.cfg.params.n_az, prob.cfg.params.n_rg), prob.scene.idx, val.astype(np.complex64))
+    return prob, op, Xin
+
+
+def test_c4_forward_adjoint_vs_oracle():
+    """Theta o G and M(Theta o .) at 32768 x 16384 vs the fp64 oracle (rel-L2 <= 1e-4)."""
+    prob, op, Xin = _c4()
+    pl = _plan(prob.cfg.params)
+    mb = mask_bits_dev(prob.mask)
+    Ag = to_host(pl.forward(to_dev(Xin), mb))
+    err = rel_l2(Ag, op.A(Xin.astype(np.complex128), prob.mask))
+    del Ag
+    assert err <= TOL_OP, err
+    AHg = to_host(pl.adjoint(to_dev(prob.Y), mb))
+    err = rel_l2(AHg, op.AH(prob.Y.astype(np.complex128), prob.mask))
+    assert err <= TOL_OP, err
+
+
+def test_c4_first_iteration_vs_oracle():
+    """Algorithm 1's first update from X = 0 at full c4 size (rel-L2 <= 1e-3; near ties excluded
+    at 1e-4)."""
+    prob, op, _ = _c4()
+    cfg = prob.cfg
+    pl = _plan(cfg.params)
+    Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr="soft", rule="k", k=cfg.k, iters=1,
+                              log=True)
+    Xg = to_host(Xg)
+    Xo, b, sig = _oracle_step(op, prob.Y.astype(np.complex128), prob.mask,
+                              np.zeros(Xg.shape, np.complex128), cfg.k)
+    assert rel_l2(Xg, Xo) <= TOL_ITA
+    keep = ~(np.abs(np.abs(b) - sig) <= NEAR * sig)
+    assert rel_l2(Xg[keep], Xo[keep]) <= TOL_OP
+    assert abs(glog[0]["sigma"] - sig) / sig <= 1e-5
+    assert glog[0]["support"] <= cfg.k
+
+
+def test_c4_teacher_forced_step():
+    """One update from the seeded late-iterate stand-in X_in (exercises S1..S5 on a nonzero
+    k-sparse state at n_az = 32768)."""
+    prob, op, Xin = _c4()
+    _teacher_forced(prob, op, _plan(prob.cfg.params), Xin, prob.cfg.k)

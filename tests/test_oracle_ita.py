@@ -246,6 +246,42 @@ def test_hard_threshold_keeps_exactly_the_top_k():
     assert np.array_equal(ita.hard(b, 0.0), b)
 
 
+def test_fixed_lambda_sigma_is_the_bruteforce_jump_point():
+    """Fixed-lambda rule (eq. 7; q = 0, 1/2, 1, 2/3 of P:L102): sigma_fixed_lambda is
+    the smallest |b| whose scalar minimiser argmin_{x>=0} (x - t)^2 + lm pen(x) is nonzero,
+    found here by brute force on dense t and x grids, with the penalty normalisation of each
+    operator's k-rule form (soft: 2 lm |x|, i.e. the 1/2 ||.||^2 scaling of R12; hard: lm 1[x != 0];
+    half: lm sqrt(x); 2/3: lm x^(2/3)) -- and lambda_from_sigma inverts it."""
+    pens = {"soft": lambda x, lm: 2.0 * lm * x, "hard": lambda x, lm: lm * (x > 0),
+            "half": lambda x, lm: lm * np.sqrt(x), "twothirds": lambda x, lm: lm * x ** (2.0 / 3.0)}
+    x = np.linspace(0.0, 6.0, 60001)
+    for thr, pen in pens.items():
+        for lam, mu in ((0.7, 1.0), (1.9, 0.6), (3.1, 1.3)):
+            lm = lam * mu
+            sig = ita.sigma_fixed_lambda(lam, mu, thr)
+            assert ita.lambda_from_sigma(sig, mu, thr) == pytest.approx(lam, rel=1e-12)
+            ts = np.linspace(0.2 * sig, 1.8 * sig, 1601)
+            nz = []
+            for t in ts:
+                xs = x[np.argmin((x - t) ** 2 + pen(x, lm))]
+                nz.append(xs > 1e-9)
+            jump = ts[np.argmax(nz)]
+            assert abs(jump - sig) <= 2.0 * (ts[1] - ts[0]), (thr, lam, mu, jump, sig)
+
+
+def test_order_statistic_matches_rank_counting():
+    """|b|_(k) against a brute-force rank count: the value v with
+    #{|b| > v} < k <= #{|b| >= v}, on data with ties and zeros."""
+    r = np.random.default_rng(5)
+    a = np.round(r.random(3000) * 50) / 7.0          # many ties
+    a[:300] = 0.0
+    b = a * np.exp(1j * r.random(3000))
+    mags = np.abs(b)
+    for k in (1, 2, 17, 299, 1500, 2699, 2700, 2701, 3000):
+        v = ita.kth_largest_mag(b, k)
+        assert np.count_nonzero(mags > v) < k <= np.count_nonzero(mags >= v), k
+
+
 def test_twothirds_matches_bruteforce_minimiser():
     """argmin_{x>=0} (x - t)^2 + lm x^(2/3) by a dense grid, lm from the k-rule sigma."""
     for sigma in (0.3, 1.0, 2.5):

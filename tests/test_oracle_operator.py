@@ -13,8 +13,9 @@ import os
 import numpy as np
 import pytest
 
+from inputs import configs
 from inputs.configs import SarParams
-from oracle import csa
+from oracle import csa, echo
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -155,3 +156,20 @@ def test_survey_transcription_anchors():
     e = g["M_ones"]
     assert abs(Mo[0, 0] - _c(e["at_0_0"])) < 2e-7
     assert abs(Mo[3, 9] - _c(e["at_3_9"])) < 2e-7
+
+
+def test_survey_exact_echo_anchors():
+    """SURVEY.md 8(c).7 exact-echo anchors: c0 system parameters (128 x 128, 60 MHz), one unit
+    target at (64, 64), N_a = 1114 aperture lines (R6): the echo sample Y[64, 64], ||Y||^2,
+    the nonzero count (the folded aperture covers every sample) and the focused M(Y)[64, 64]."""
+    g = json.load(open(os.path.join(GOLD, "survey_8c7_anchors.json")))["c0_echo_unit_target_64_64"]
+    p = configs.get("c0").params
+    assert echo.aperture_lines(p) == 1114
+    Y = echo.exact_echo(p, [(64, 64, 1.0 + 0j)])
+    # the echo phase carries a ~3e7-cycle carrier: fp64 rounding of its argument ~5e-8 rad per term
+    assert abs(Y[64, 64] - _c(g["Y_64_64"])) <= 1e-6 * abs(_c(g["Y_64_64"]))
+    assert float(np.vdot(Y, Y).real) == pytest.approx(g["norm2"], rel=1e-8)
+    assert int(np.count_nonzero(Y)) == g["nonzeros"]
+    MY = csa.CSAOperator(p).M(Y)
+    assert abs(MY[64, 64] - _c(g["MY_64_64"])) <= 1e-7 * g["MY_64_64_abs"]
+    assert abs(MY[64, 64]) == pytest.approx(g["MY_64_64_abs"], rel=1e-9)
