@@ -85,7 +85,7 @@ typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 
  * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
  * accumulates per-step device time (read with cssar_stage_times). */
 enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPARSE_X = 4,
-       CSSAR_FLAG_PEER_TRANSPOSE = 8 };
+       CSSAR_FLAG_PEER_TRANSPOSE = 8, CSSAR_FLAG_SPARSE_STATE = 16 };
 
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
  * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule.
@@ -99,6 +99,14 @@ enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPA
  * array (the kept X_i); per iteration one more elementwise pass (X_(i+1) vs X_i, 24 B/sample)
  * and a host synchronisation on `stream`.  The number of updates performed is read with
  * cssar_ita_iters_done; log entries exist only for those.
+ * CSSAR_FLAG_SPARSE_STATE (a request; NEXT-3; applies to world 1, k-rule, fixed mu, tol = 0,
+ * n_az >= 2048, iters >= 2): from iteration 1 on the state between iterations is, per column
+ * panel of the azimuth sweeps, the list of b entries at or above the select's candidate
+ * window (X_i = E(b_(i-1)) is k-sparse) kept in the workspace instead of a dense b
+ * in X_inout: S5 writes no dense b and S1 reads no dense b (72 instead of 96 B/sample per
+ * iteration).  A select fallback re-runs S5 densely into X_inout.  Same results as the dense
+ * schedule (bitwise).  Not the default: the sweeps are latency-bound, and on B200 the list
+ * fills cost more than the dense b traffic they save.
  * CSSAR_FLAG_PEER_TRANSPOSE (world > 1; a request): the fused transposes -- sweep epilogues
  * store straight into the peers' slabs through the CUDA-IPC mappings made at bind time, a
  * device flag barrier (system-scope release/acquire on slots in every rank's workspace, 20 s
@@ -167,7 +175,8 @@ int cssar_nccl_unique_id(void* id_out);
 
 /* Bytes of device workspace cssar_ita_iterate needs: world 1: three complex64 arrays of the
  * scene size (transform buffer; adaptive-step gradient; X_i of the tolerance stop) plus a
- * candidate buffer for the exact top-k select (~24.5 B/sample); world > 1:
+ * candidate buffer for the exact top-k select (~24.5 B/sample), and for n_az >= 2048 the two
+ * sparse-state lists (16-byte entries, room for every sample: +32 B/sample); world > 1:
  * four complex64 column-slab arrays (transposes, Y, state), the column-slab mask and the
  * candidate buffer (~32.6 B per local sample). */
 int cssar_workspace_size(cssar_plan plan, size_t* bytes);

@@ -13,7 +13,7 @@ LIB = os.path.join(HERE, "libcssar.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-SOURCES = ["api.cu", "rg.cu", "select.cu", "az_host.cu", "step.cu", "sparse.cu", "peer.cu"] + [f"az_{l}.cu" for l in range(7, 16)]
+SOURCES = ["api.cu", "rg.cu", "select.cu", "az_host.cu", "step.cu", "sparse.cu", "peer.cu", "ss.cu"] + [f"az_{l}.cu" for l in range(7, 16)]
 
 
 def _obj(src):

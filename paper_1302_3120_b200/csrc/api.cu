@@ -108,6 +108,9 @@ struct cssar_plan_s {
   uint32_t* h_nonfinite = nullptr;
   cudaEvent_t ev_solve = nullptr;
   bool solve_pending = false;
+  // sparse-state schedule (world 1, cluster azimuth shapes): two per-panel lists in the workspace
+  SsLists ss{};
+  bool ss_ok = false;
 };
 
 namespace {
@@ -334,9 +337,27 @@ int enqueue_adjoint(cssar_plan pl, const void* R, const uint32_t* mask, void* Xo
   return CSSAR_OK;
 }
 
+// S6 of the sparse-state schedule: coarse select; on a fallback the dense S5 re-run into b, the
+// full-histogram kernels and the fine select on it, then the list rebuild (each early-exits
+// unless the coarse select asked for the fallback)
+cudaError_t launch_select_ss(cssar_plan pl, AzArgs a, float2* b, const cssar_ita_params& prm, cudaStream_t s) {
+  cudaError_t e = launch_select_part(SEL_COARSE, pl->sm_count, b, pl->n, prm.k, prm.thr, (float)prm.mu, pl->d_st,
+                                     pl->d_hist, pl->d_hist_full, pl->cand, pl->cand_cap, pl->d_lvl, pl->d_log, kLogCap,
+                                     s);
+  if (e != cudaSuccess) return e;
+  a.in = pl->U;
+  a.b = b;
+  e = launch_az(pl->log_naz, AZ_TAIL_SSD, a.n_rg, a, s);
+  if (e != cudaSuccess) return e;
+  e = launch_select_rest(pl->sm_count, b, pl->n, prm.k, prm.thr, (float)prm.mu, pl->d_st, pl->d_hist,
+                         pl->d_hist_full, pl->cand, pl->cand_cap, pl->d_log, kLogCap, s);
+  if (e != cudaSuccess) return e;
+  return launch_ss_rebuild(b, (int)pl->p.n_az, (int)pl->p.n_rg, pl->ss, pl->d_st, 0, s);
+}
+
 // one ITA iteration (S1..S6) on stream s
 int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const cssar_ita_params& prm, void* X,
-                      cudaStream_t s, bool prof = false) {
+                      cudaStream_t s, bool prof = false, bool ss = false) {
   // PROFILE_STAGES: CUDA events between the steps, and NVTX ranges S1..S6 for nsys timelines
   static const char* const kStage[6] = {"S1 az head", "S2 range G", "S3 az residual", "S4 range M", "S5 az tail",
                                          "S6 select"};
@@ -365,15 +386,16 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   a.mask = mask;
   a.red_part = pl->d_red;
   a.red_ticket = reinterpret_cast<uint32_t*>(pl->d_red + 3 * kRedSlots);
+  a.ss = pl->ss;
   float2* b = (float2*)X;
   RgArgs r{pl->U, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
   r.hrange = pl->d_hrange;
   MARK(0);
-  // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta
-  a.in = b;
+  // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta   (sparse state: b_{i-1} from the list)
+  a.in = ss ? pl->U : b;                 // (FWD_SS reads no dense input; any mapped pointer)
   a.out = pl->U;
-  CUDA_TRY(launch_az(pl->log_naz, AZ_FWD_THR, a.n_rg, a, s));
+  CUDA_TRY(launch_az(pl->log_naz, ss ? AZ_FWD_SS : AZ_FWD_THR, a.n_rg, a, s));
   MARK(1);
   // S2: G body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
@@ -402,14 +424,24 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
     CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
     CUDA_TRY(launch_az(pl->log_naz, AZ_NORM, a.n_rg, a, s));
     CUDA_TRY(launch_adaptive_step(a, pl->n, pl->sm_count, s));
+  } else if (ss) {
+    // S5 (sparse state): X_i from the list; b_i -> histogram, candidates and the next list
+    a.in = pl->U;
+    CUDA_TRY(launch_az(pl->log_naz, AZ_TAIL_SS, a.n_rg, a, s));
   } else {
     // S5: F_eta^-1 ; b_i = X_i + mu dX ; |b|^2 histogram + candidates
     CUDA_TRY(launch_az(pl->log_naz, AZ_TAIL, a.n_rg, a, s));
   }
   MARK(5);
   // S6: sigma_i (k-rule select or fixed lambda)
-  CUDA_TRY(launch_select(pl->sm_count, b, pl->n, prm.k, prm.rule, prm.thr, (float)prm.mu, pl->d_st, pl->d_hist,
-                         pl->d_hist_full, pl->cand, pl->cand_cap, pl->d_log, kLogCap, s));
+  if (ss) {
+    // select fallback (target bin outside the window): S5 again with a dense b_i in X's buffer
+    // for the full-histogram kernels (early exit otherwise), then the list rebuilt from it
+    CUDA_TRY(launch_select_ss(pl, a, b, prm, s));
+  } else {
+    CUDA_TRY(launch_select(pl->sm_count, b, pl->n, prm.k, prm.rule, prm.thr, (float)prm.mu, pl->d_st, pl->d_hist,
+                           pl->d_hist_full, pl->cand, pl->cand_cap, pl->d_log, kLogCap, s));
+  }
   MARK(6);
 #undef MARK
   return CSSAR_OK;
@@ -1119,8 +1151,18 @@ size_t cand_capacity(long long n) { return (size_t)(n / 8 + 65536); }
 // sparse-X' list of a world > 1 rank: kSxHeader-byte header (count) + nl/8 entries of 16 bytes
 size_t sx_bytes(size_t nl) { return align256(kSxHeader + sizeof(SxEntry) * (nl / 8)); }
 
+// sparse-state lists of a world-1 plan with cluster azimuth shapes: 2 x (a full-panel entry
+// array per panel + its counter)
+size_t ss_bytes(cssar_plan pl) {
+  const int W = az_panel_width(pl->log_naz);
+  if (pl->world != 1 || W <= 0) return 0;
+  const size_t npan = (size_t)(pl->p.n_rg / W);
+  return 2 * (align256(sizeof(SsEntry) * (size_t)pl->n) + align256(sizeof(uint32_t) * npan));
+}
+
 size_t workspace_bytes(cssar_plan pl) {
-  if (pl->world == 1) return 3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n) + 256;
+  if (pl->world == 1)
+    return align256(3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n)) + ss_bytes(pl) + 256;
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
   return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + align256(sizeof(uint32_t) * cand_capacity((long long)nl)) +
          256 + sx_bytes(nl) + 256;
@@ -1133,6 +1175,21 @@ void bind_views(cssar_plan pl, char* ws) {
     pl->Xk = (float2*)(ws + 2 * sizeof(float2) * (size_t)pl->n);
     pl->cand = (uint32_t*)(ws + 3 * sizeof(float2) * (size_t)pl->n);
     pl->cand_cap = (uint32_t)cand_capacity(pl->n);
+    pl->ss = SsLists{};
+    pl->ss_ok = ss_bytes(pl) > 0;
+    if (pl->ss_ok) {
+      char* q = ws + align256(3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n));
+      const int W = az_panel_width(pl->log_naz);
+      pl->ss.W = W;
+      pl->ss.npan = (int)(pl->p.n_rg / W);
+      pl->ss.capp = (uint32_t)(pl->p.n_az * W);
+      for (int l = 0; l < 2; ++l) {
+        pl->ss.ent[l] = reinterpret_cast<SsEntry*>(q);
+        q += align256(sizeof(SsEntry) * (size_t)pl->n);
+        pl->ss.cnt[l] = reinterpret_cast<uint32_t*>(q);
+        q += align256(sizeof(uint32_t) * (size_t)pl->ss.npan);
+      }
+    }
     return;
   }
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
@@ -1366,6 +1423,20 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   CUDA_TRY(launch_init_state(pl->d_st, pl->d_hist, pl->d_hist_full, prm->thr, sigma_fixed, s));
   const bool prof = (prm->flags & CSSAR_FLAG_PROFILE_STAGES) != 0;
   const bool tol = prm->tol > 0.0;
+  // sparse-state schedule (NEXT-3, CSSAR_FLAG_SPARSE_STATE): k-rule, fixed step, no tolerance
+  // stop, cluster azimuth shapes; iteration 0 (arbitrary X_0) runs dense and its b_0 seeds the list
+  const bool ss = pl->ss_ok && prm->rule == CSSAR_RULE_KSPARSE && !(prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && !tol &&
+                  (prm->flags & CSSAR_FLAG_SPARSE_STATE) && prm->iters >= 2;
+  if (ss) {
+    for (int l = 0; l < 2; ++l)
+      CUDA_TRY(cudaMemsetAsync(pl->ss.cnt[l], 0, sizeof(uint32_t) * (size_t)pl->ss.npan, s));
+    CUDA_TRY(launch_ss_set(pl->d_st, pl->ss.cnt[0], pl->ss.cnt[1], pl->ss.npan, s));
+  }
+  // sparse state after the dense iteration 0: the list from b_0 (the select has set sigma_0)
+  auto ss_seed = [&]() -> int {
+    CUDA_TRY(launch_ss_rebuild((const float2*)X_inout, (int)pl->p.n_az, (int)pl->p.n_rg, pl->ss, pl->d_st, 1, s));
+    return CSSAR_OK;
+  };
   if (tol) {                                   // X_0 = E(b; sigma_init) = X_inout
     if (!pl->d_conv) {
       pl->conv_blocks = 4 * pl->sm_count;
@@ -1391,8 +1462,9 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
     for (int i = 0; i < 6; ++i) pl->stage_ms[i] = 0.0;
     pl->stage_iters = 0;
     for (int it = 0; it < prm->iters; ++it) {
-      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, true);
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, true, ss && it > 0);
       if (rc != CSSAR_OK) return rc;
+      if (ss && it == 0 && (rc = ss_seed()) != CSSAR_OK) return rc;
       CUDA_TRY(cudaEventSynchronize(pl->ev[6]));
       for (int i = 0; i < 6; ++i) {
         float ms = 0.f;
@@ -1406,14 +1478,21 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       if (stop) break;
     }
   } else if (prm->iters > 0) {
+    int first = 0;
+    if (ss) {                                  // iteration 0: dense, outside the graph
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s);
+      if (rc != CSSAR_OK) return rc;
+      if ((rc = ss_seed()) != CSSAR_OK) return rc;
+      first = 1;
+    }
     GraphKey key{Y, mask_bits, X_inout, prm->thr, prm->rule, prm->rule == CSSAR_RULE_KSPARSE ? prm->k : 0,
-                 prm->lambda, prm->mu, prm->flags & CSSAR_FLAG_ADAPTIVE_MU};
+                 prm->lambda, prm->mu, (prm->flags & CSSAR_FLAG_ADAPTIVE_MU) | (ss ? CSSAR_FLAG_SPARSE_STATE << 8 : 0)};
     if (!pl->ghave || !(pl->gkey == key)) {
       if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
       pl->ghave = false;
       cudaGraph_t g = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
-      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, pl->cap_stream);
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, pl->cap_stream, false, ss);
       cudaError_t ec = cudaStreamEndCapture(pl->cap_stream, &g);
       if (rc != CSSAR_OK) { if (g) cudaGraphDestroy(g); return rc; }
       CUDA_TRY(ec);
@@ -1423,7 +1502,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       pl->gkey = key;
       pl->ghave = true;
     }
-    for (int it = 0; it < prm->iters; ++it) {
+    for (int it = first; it < prm->iters; ++it) {
       CUDA_TRY(cudaGraphLaunch(pl->gexec, s));
       bool stop = false;
       const int rc = converged(it, stop);
@@ -1431,7 +1510,10 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       if (stop) break;
     }
   }
-  CUDA_TRY(launch_finalize((float2*)X_inout, pl->n, prm->thr, pl->d_st, s));
+  if (ss)                                      // X_I from the last list
+    CUDA_TRY(launch_ss_finalize((float2*)X_inout, (int)pl->p.n_az, (int)pl->p.n_rg, pl->ss, prm->thr, pl->d_st, s));
+  else
+    CUDA_TRY(launch_finalize((float2*)X_inout, pl->n, prm->thr, pl->d_st, s));
   CUDA_TRY(note_solve_end(pl, s));
   if (log_host) {
     const int nl = pl->iters_done;

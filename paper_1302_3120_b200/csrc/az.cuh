@@ -66,7 +66,9 @@ struct AzCfg<13, true> {
 };
 #endif
 
-template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true, bool DEF = false>
+constexpr int kSlCap = 512;      // sparse-state tail: list entries staged in SMEM per panel
+
+template <int LOGN, bool R = false, int NSO = 0, bool TAILM = true, bool DEF = false, bool SSB = false>
 struct AzShape {
   using P = AzCfg<LOGN, R>;
   static constexpr int C = P::C, W = P::W, E = P::E, NS = NSO > 0 ? NSO : P::NS;
@@ -98,18 +100,45 @@ struct AzShape {
   static constexpr size_t CL_CTW_OFF = CL_TW_OFF + ((sizeof(float2) * TWK + 15) / 16) * 16;
   static constexpr size_t CL_BAR_OFF = CL_CTW_OFF + sizeof(float2) * CTW;
   static constexpr size_t CL_MISC_OFF = CL_BAR_OFF + 8 * NS + 24 + 8;
-  static constexpr size_t CL_SMEM = 1024 + CL_MISC_OFF + sizeof(uint32_t) * (64 + (TAILM ? HIST_BINS + CAND_SMEM + 4 : 0));
+  // sparse-state tail: SMEM staging of the new list entries of a panel (flushed per panel)
+  static constexpr int SL_CAP = kSlCap;
+  static constexpr size_t CL_SL_OFF =
+      ((CL_MISC_OFF + sizeof(uint32_t) * (64 + (TAILM ? HIST_BINS + CAND_SMEM + 4 : 0)) + 15) / 16) * 16;
+  static constexpr size_t CL_SMEM = 1024 + CL_SL_OFF + (SSB ? sizeof(SsEntry) * SL_CAP : 0);
   static constexpr int CL_MINB = T <= 128 ? 3 : T <= 256 ? 2 : 1;
 };
 
 struct TailCtx {
   uint32_t* shist;
   uint32_t* scand;
-  uint32_t* scount;      // [0] = candidates in SMEM, [1] = fixed-lambda survivors
+  uint32_t* scount;      // [0] = candidates in SMEM, [1] = fixed-lambda survivors, [2] = list entries in SMEM
   int floor_bin, cand_lo, cand_hi;
   uint32_t s2bits, s2fixed;
   float sigma;
+  // sparse-state tail: new list entries (|b|^2 >= list_floor) of the current panel
+  SsEntry* sl_buf;
+  SsEntry* went;         // write list entries (panel-major) and counters
+  uint32_t* wcnt;
+  uint32_t list_floor;
+  uint32_t capp;
+  int panel, col0;
 };
+
+// one new list entry of the sparse-state tail: staged in SMEM, overflow straight to the list
+template <int SL_CAP>
+CSSAR_DEV void ss_push(TailCtx& tc, int row, int col, float2 v) {
+  SsEntry e;
+  e.row = (uint32_t)row;
+  e.w = (uint32_t)(col - tc.col0);
+  e.v = v;
+  const uint32_t pos = atomicAdd(&tc.scount[2], 1u);
+  if (pos < (uint32_t)SL_CAP) {
+    tc.sl_buf[pos] = e;
+  } else {
+    const uint32_t g = atomicAdd(&tc.wcnt[tc.panel], 1u);
+    tc.went[(size_t)tc.panel * tc.capp + g] = e;
+  }
+}
 
 // auxiliary per-element inputs, fetched for a whole group before any arithmetic so the
 // loads are in flight together (long-scoreboard latency overlaps)
@@ -151,7 +180,7 @@ CSSAR_DEV void red_commit(double* part, uint32_t* ticket, double* target, float 
 
 template <int MODE>
 struct AzOps {
-  static constexpr int DIR = (MODE <= AZ_FWD_THR) ? -1 : +1;   // first transform direction
+  static constexpr int DIR = (MODE <= AZ_FWD_THR || MODE == AZ_FWD_SS) ? -1 : +1;   // first transform direction
   // kernels that reduce a squared norm into the solver state
   static constexpr bool RED = MODE == AZ_RESID || MODE == AZ_GRAD || MODE == AZ_NORM;
   CSSAR_DEV static double* red_target(const AzArgs& a) {
@@ -167,7 +196,7 @@ struct AzOps {
     if constexpr (MODE == AZ_FWD_MASK) {
       if (!mask_bit(a.mask, a.mask_words, row, col)) v = make_float2(0.f, 0.f);
     }
-    if constexpr (MODE == AZ_FWD_THR) v = threshold(v, s2, sig, a.thr);
+    if constexpr (az_is_thr(MODE)) v = threshold(v, s2, sig, a.thr);
     return v;
   }
 
@@ -235,13 +264,19 @@ struct AzOps {
     if constexpr (MODE == AZ_NORM) {
       acc = fmaf(v0.x, v0.x, fmaf(v0.y, v0.y, acc));
       acc = fmaf(v1.x, v1.x, fmaf(v1.y, v1.y, acc));
-    } else if constexpr (MODE == AZ_TAIL) {
+    } else if constexpr (az_is_tail(MODE)) {
       const float2 k0 = threshold(a0.v, tc.s2bits, tc.sigma, a.thr), k1 = threshold(a1.v, tc.s2bits, tc.sigma, a.thr);
       v0 = make_float2(fmaf(a.mu, v0.x, k0.x), fmaf(a.mu, v0.y, k0.y));
       v1 = make_float2(fmaf(a.mu, v1.x, k1.x), fmaf(a.mu, v1.y, k1.y));
-      *reinterpret_cast<float4*>(a.b + idx) = make_float4(v0.x, v0.y, v1.x, v1.y);
-      tail_stats(a, v0, tc);
-      tail_stats(a, v1, tc);
+      if constexpr (MODE != AZ_TAIL_SS) *reinterpret_cast<float4*>(a.b + idx) = make_float4(v0.x, v0.y, v1.x, v1.y);
+      if constexpr (MODE != AZ_TAIL_SSD) {
+        tail_stats(a, v0, tc);
+        tail_stats(a, v1, tc);
+      }
+      if constexpr (MODE == AZ_TAIL_SS) {
+        if (mag2_bits(v0) >= tc.list_floor) ss_push<kSlCap>(tc, row, col, v0);
+        if (mag2_bits(v1) >= tc.list_floor) ss_push<kSlCap>(tc, row, col + 1, v1);
+      }
     } else {
       *reinterpret_cast<float4*>(out_at(a, row, col)) = make_float4(v0.x, v0.y, v1.x, v1.y);
     }
@@ -277,11 +312,14 @@ struct AzOps {
     }
     if constexpr (MODE == AZ_NORM) {
       acc = fmaf(v.x, v.x, fmaf(v.y, v.y, acc));
-    } else if constexpr (MODE == AZ_TAIL) {
+    } else if constexpr (az_is_tail(MODE)) {
       const float2 xk = threshold(ax.v, tc.s2bits, tc.sigma, a.thr);     // X_i recomputed
       const float2 bn = make_float2(fmaf(a.mu, v.x, xk.x), fmaf(a.mu, v.y, xk.y));
-      a.b[idx] = bn;
-      tail_stats(a, bn, tc);
+      if constexpr (MODE != AZ_TAIL_SS) a.b[idx] = bn;
+      if constexpr (MODE != AZ_TAIL_SSD) tail_stats(a, bn, tc);
+      if constexpr (MODE == AZ_TAIL_SS) {
+        if (mag2_bits(bn) >= tc.list_floor) ss_push<kSlCap>(tc, row, col, bn);
+      }
     } else {
       *out_at(a, row, col) = v;
     }
@@ -466,6 +504,9 @@ CSSAR_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 // lo[l] = w_N^l, hi[h] = w_N^{h 2^LO} (one product: at most ~1.5 ulp, no recurrences)
 template <int C, int DIR, int LOGN, int LO>
 CSSAR_DEV void cluster_twiddles(float2* x, uint32_t k, const float2* ctw) {
+#if defined(CSSAR_EXP_NOFFT_AZ)
+  return;
+#endif
   constexpr uint32_t NM = (1u << LOGN) - 1u, LM = (1u << LO) - 1u;
 #pragma unroll
   for (int c = 1; c < C; ++c) {
@@ -477,6 +518,9 @@ CSSAR_DEV void cluster_twiddles(float2* x, uint32_t k, const float2* ctw) {
 
 template <int C, int DIR, int LOGN, int LO>
 CSSAR_DEV void cluster_twiddles2(float2* x, float2* y, uint32_t k, const float2* ctw) {
+#if defined(CSSAR_EXP_NOFFT_AZ)
+  return;
+#endif
   constexpr uint32_t NM = (1u << LOGN) - 1u, LM = (1u << LO) - 1u;
 #pragma unroll
   for (int c = 1; c < C; ++c) {
@@ -487,8 +531,22 @@ CSSAR_DEV void cluster_twiddles2(float2* x, float2* y, uint32_t k, const float2*
   }
 }
 
+// the radix-C DFT across the cluster's partial transforms
+template <int C, int DIR>
+CSSAR_DEV void cl_dft(float2 (&z)[C]) {
+#if !defined(CSSAR_EXP_NOFFT_AZ)
+  dft_sr<C, DIR>(z);
+#endif
+}
+
 // async DSMEM store that signals the destination CTA's mbarrier (same SMEM offset mapped)
+#if defined(CSSAR_EXP_NOPUSH_AZ)
+constexpr bool kNoPush = true;      // experiment: no DSMEM exchange (values dropped, no peer waits)
+#else
+constexpr bool kNoPush = false;
+#endif
 CSSAR_DEV void st_async_cluster(uint32_t raddr, float2 v, uint32_t rbar) {
+  if (kNoPush) return;
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
                "f"(v.x), "f"(v.y), "r"(rbar)
                : "memory");
@@ -514,10 +572,11 @@ template <int MODE>
 constexpr bool kAzDefer = false;
 #else
 template <int MODE>
-constexpr bool kAzDefer = MODE == AZ_FWD_THR;
+constexpr bool kAzDefer = az_is_thr(MODE);
 #endif
 template <int LOGN, int MODE>
-using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, MODE == AZ_TAIL, kAzDefer<MODE>>;
+using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, az_is_tail(MODE), kAzDefer<MODE>,
+                          MODE == AZ_TAIL_SS>;
 
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE>::CL_MINB)
@@ -529,7 +588,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   constexpr bool RES = MODE == AZ_RESID || MODE == AZ_GRAD;   // two transforms, scatter
   // BS (TAIL, one stage): b_{i-1} of the output rows arrives by TMA into the stage buffer once the
   // local transform has read it; the next panel's stage load is issued after the epilogue
-  constexpr bool BS = MODE == AZ_TAIL && NS == 1;
+  constexpr bool BS = az_is_tail(MODE) && NS == 1;
+  constexpr bool SSR = az_is_ss(MODE);      // input state from the list (no dense b)
   // PP (RESID/GRAD with XS, TAIL with BS): the stage and the receive buffer swap roles every
   // panel, so the next panel's TMA load goes into the receive buffer as soon as it is consumed
   // (mid-panel) instead of into the stage after the panel's last use of it; the cluster arrive
@@ -539,7 +599,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #else
   constexpr bool PP = (RES && Cf::XS) || BS;
 #endif
-  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && !BS) || MODE == AZ_INV_MASK ||
+  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (az_is_tail(MODE) && !BS) || MODE == AZ_INV_MASK ||
                       MODE == AZ_NORM;
   static_assert(C > 1, "cluster kernel");
   constexpr bool DEFER = kAzDefer<MODE> && !RES && !AUX && !BS && NS == 1;
@@ -587,8 +647,15 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     const uint32_t m = i < (1 << Cf::LO) ? (uint32_t)i : (uint32_t)(i - (1 << Cf::LO)) << Cf::LO;
     ctw[i] = expi_frac<-1>(m, (uint32_t)N);
   }
+  pdl_wait();                                     // the previous kernel's output and state are complete
+  if constexpr (MODE == AZ_TAIL_SSD) {
+    if (!a.st->need_full) return;               // fallback re-run only (uniform over the grid)
+  }
+  // sparse-state lists: read the one the previous S5 (or the rebuild) wrote, write the other
+  const int ss_rd = SSR ? ((a.st->iter + 1) & 1) : 0;
+  const int ss_wr = SSR ? (a.st->iter & 1) : 0;
   TailCtx tc{};
-  if constexpr (MODE == AZ_TAIL) {
+  if constexpr (az_is_tail(MODE)) {
     tc.shist = misc + 64;
     tc.scand = tc.shist + HIST_BINS;
     tc.scount = tc.scand + Cf::CAND_SMEM;
@@ -600,10 +667,52 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     tc.s2bits = a.st->sigma2_bits;
     tc.s2fixed = a.st->sigma2_fixed_bits;
     tc.sigma = a.st->sigma;
+    if constexpr (MODE == AZ_TAIL_SS) {
+      // entries that can exceed any sigma_i the window select can return (bins >= cand_lo)
+      tc.sl_buf = reinterpret_cast<SsEntry*>(base + Cf::CL_SL_OFF);
+      tc.went = a.ss.ent[ss_wr];
+      tc.wcnt = a.ss.cnt[ss_wr];
+      tc.capp = a.ss.capp;
+      tc.list_floor = tc.cand_lo > 0 ? (uint32_t)tc.cand_lo << HIST_SHIFT : 0u;
+    }
   }
+  // sparse-state input: zero the SMEM block and scatter the panel's list entries into it.
+  //   FWD_SS : the stage rows rank + C m   -> s[m W + w]
+  //   TAIL_SS: the output rows k + M q (k in this rank's M/C block) -> s[(q M/C + k mod M/C) W + w]
+  // Split so the list loads overlap other work: ss_zero_prefetch (block free: zero it, load the
+  // first kSsPf entries per thread into registers) ... __syncthreads ... ss_scatter.
+  constexpr int kSsPf = 4;
+  SsEntry pf[kSsPf];
+  uint32_t pf_n = 0;
+  int pf_panel = 0;
+  auto ss_place = [&](float2* dst, const SsEntry& x) {
+    if constexpr (MODE == AZ_FWD_SS) {
+      if ((int)(x.row % C) == rank) dst[(x.row / C) * W + x.w] = x.v;
+    } else {
+      const uint32_t q = x.row / M, k = x.row % M;
+      if ((int)(k / (M / C)) == rank) dst[(q * (M / C) + k % (M / C)) * W + x.w] = x.v;
+    }
+  };
+  auto ss_zero_prefetch = [&](int panel, float2* dst) {
+    pf_panel = panel;
+    pf_n = a.ss.cnt[ss_rd][panel];
+    const SsEntry* e = a.ss.ent[ss_rd] + (size_t)panel * a.ss.capp;
+#pragma unroll
+    for (int j = 0; j < kSsPf; ++j)
+      if ((uint32_t)(t + j * T) < pf_n) pf[j] = e[t + j * T];
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int i = t; i < M * W / 2; i += T) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto ss_scatter = [&](float2* dst) {          // after a __syncthreads that follows the zeroing
+#pragma unroll
+    for (int j = 0; j < kSsPf; ++j)
+      if ((uint32_t)(t + j * T) < pf_n) ss_place(dst, pf[j]);
+    const SsEntry* e = a.ss.ent[ss_rd] + (size_t)pf_panel * a.ss.capp;
+    for (uint32_t i = t + kSsPf * T; i < pf_n; i += T) ss_place(dst, e[i]);
+  };
   uint32_t s2 = 0u;
   float sig = 0.f;
-  if constexpr (MODE == AZ_FWD_THR || MODE == AZ_GRAD) {
+  if constexpr (az_is_thr(MODE) || MODE == AZ_GRAD) {
     s2 = a.st->sigma2_bits;
     sig = a.st->sigma;
   }
@@ -627,12 +736,14 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     mbar_init(rfull, 1u);
     mbar_init(xfull, 1u);
     mbar_init(yfull, 1u);
-    mbar_expect_tx(rfull, Cf::STAGE_BYTES);        // armed for the first panel
-    if (RES || DEFER) mbar_expect_tx(xfull, Cf::STAGE_BYTES);   // DEFER: xfull = second receive buffer
+    if (!kNoPush) mbar_expect_tx(rfull, Cf::STAGE_BYTES);        // armed for the first panel
+    if ((RES || DEFER) && !kNoPush) mbar_expect_tx(xfull, Cf::STAGE_BYTES);   // DEFER: xfull = second receive buffer
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    for (int i = 0; i < NS; ++i)
-      if (cid + i * ncl < npan) issue(cid + i * ncl, i, stages + (size_t)i * M * W);
+    if constexpr (MODE != AZ_FWD_SS) {
+      for (int i = 0; i < NS; ++i)
+        if (cid + i * ncl < npan) issue(cid + i * ncl, i, stages + (size_t)i * M * W);
+    }
   }
   __syncthreads();
   // barrier initialisation visible cluster-wide before any remote st.async (once per kernel)
@@ -643,8 +754,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     if constexpr (DEFER) {
       float2* rb = rbuf0 + ((pit & 1) ? (size_t)M * W : 0);
       uint64_t* rbar = (pit & 1) ? xfull : rfull;
-      mbar_wait_cta(rbar, (uint32_t)((pit >> 1) & 1));
-      if (t == 0) mbar_expect_tx(rbar, Cf::STAGE_BYTES);
+      if (!kNoPush) mbar_wait_cta(rbar, (uint32_t)((pit >> 1) & 1));
+      if (t == 0 && !kNoPush) mbar_expect_tx(rbar, Cf::STAGE_BYTES);
       float2 z[PT][C];
 #pragma unroll
       for (int p = 0; p < PT; p += 2) {
@@ -656,8 +767,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           z[p + 1][c] = make_float2(q.z, q.w);
         }
         cluster_twiddles2<C, Ops::DIR, LOGN, Cf::LO>(z[p], z[p + 1], (uint32_t)slot_k(p), ctw);
-        dft_sr<C, Ops::DIR>(z[p]);
-        dft_sr<C, Ops::DIR>(z[p + 1]);
+        cl_dft<C, Ops::DIR>(z[p]);
+        cl_dft<C, Ops::DIR>(z[p + 1]);
       }
       consume(z, misc + 40);
       cl_arrive();                                 // this receive buffer consumed
@@ -672,6 +783,9 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     }
   };
   int it = 0;
+  if constexpr (MODE == AZ_FWD_SS) {
+    if (cid < npan) ss_zero_prefetch(cid, stages);
+  }
   for (int panel = cid; panel < npan; panel += ncl, ++it) {
     const int sidx = it % NS;
     float2* s = stages + (size_t)sidx * M * W;
@@ -684,6 +798,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     }
     const int col0 = panel * W;
     const int next = panel + NS * ncl;
+    if constexpr (MODE == AZ_TAIL_SS) {
+      tc.panel = panel;
+      tc.col0 = col0;
+    }
     // epilogue / residual inputs of output rows k + M q (in flight during the FFT)
     Aux ax[PT][C];
     if constexpr (AUX) {
@@ -732,7 +850,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     }
-    mbar_wait_cta(&full[sidx], (uint32_t)((it / NS) & 1));
+    if constexpr (MODE == AZ_FWD_SS) {
+      __syncthreads();                             // the stage zeroed (previous refill point)
+      ss_scatter(s);                               // the stage from the state list (no TMA)
+      __syncthreads();
+    } else {
+      mbar_wait_cta(&full[sidx], (uint32_t)((it / NS) & 1));
+    }
     // local transform of rows rank + C m (stage layout [m][w] = engine BMINOR layout)
     auto ld = [&](int w, int j, float2* x) {
 #pragma unroll
@@ -743,7 +867,10 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     float2 v[E];
     En::template run_keep<Ops::DIR>(s, v, ld, tw);
     float2* const xbuf = Cf::XS ? s : xbuf0;
-    if constexpr (BS) {
+    if constexpr (BS && SSR) {
+      __syncthreads();                             // stage read: b_{i-1} of the output rows from the list
+      ss_zero_prefetch(panel, s);                  // (scattered after the cross-CTA step)
+    } else if constexpr (BS) {
       __syncthreads();                             // stage read: bring in b_{i-1} of the output rows
       if (t == 0) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -761,7 +888,9 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       }
     } else if constexpr (!Cf::XS) {
       __syncthreads();                             // stage fully read: refill it NS panels ahead
-      if (t == 0 && next < npan) {
+      if constexpr (MODE == AZ_FWD_SS) {
+        if (next < npan) ss_zero_prefetch(next, s);
+      } else if (t == 0 && next < npan) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         issue(next, sidx, s);
       }
@@ -785,8 +914,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       else cl_arrive();                            // (the second receive buffer is free)
       continue;
     }
-    mbar_wait_cta(rfull, (uint32_t)(it & 1));      // all C partial transforms of our block landed
-    if (t == 0) mbar_expect_tx(rfull, Cf::STAGE_BYTES);   // re-arm for the next panel
+    if (!kNoPush) mbar_wait_cta(rfull, (uint32_t)(it & 1));      // all C partial transforms of our block landed
+    if (t == 0 && !kNoPush) mbar_expect_tx(rfull, Cf::STAGE_BYTES);   // re-arm for the next panel
     float2 z[PT][C];
     if constexpr (VEC) {
 #pragma unroll
@@ -799,8 +928,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
           z[p + 1][c] = make_float2(q.z, q.w);
         }
         cluster_twiddles2<C, Ops::DIR, LOGN, Cf::LO>(z[p], z[p + 1], (uint32_t)slot_k(p), ctw);
-        dft_sr<C, Ops::DIR>(z[p]);
-        dft_sr<C, Ops::DIR>(z[p + 1]);
+        cl_dft<C, Ops::DIR>(z[p]);
+        cl_dft<C, Ops::DIR>(z[p + 1]);
       }
     } else {
 #pragma unroll
@@ -813,7 +942,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
       for (int p = 0; p < PT; ++p) {
         const int k = slot_k(p);
         cluster_twiddles<C, Ops::DIR, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);   // w_N^{c k}
-        dft_sr<C, Ops::DIR>(z[p]);                                       // z[q] = X[k + M q]
+        cl_dft<C, Ops::DIR>(z[p]);                                       // z[q] = X[k + M q]
       }
     }
     consume(z, misc + 40);
@@ -824,6 +953,11 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         issue(next, sidx, rbuf);
       }
+    }
+    if constexpr (BS && SSR) {                     // b_{i-1} of the output rows (zeroed at the
+      if constexpr (!PP) __syncthreads();          //  local transform's end; synced above)
+      ss_scatter(s);
+      __syncthreads();
     }
     if constexpr (RES) {
 #pragma unroll
@@ -836,7 +970,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
         const int pr = p * T + t;
         const int k = rank * (M / C) + pr / W;
-        dft_sr<C, -1>(z[p]);                                           // forward DIF first stage
+        cl_dft<C, -1>(z[p]);                                           // forward DIF first stage
         cluster_twiddles<C, -1, LOGN, Cf::LO>(z[p], (uint32_t)k, ctw);     // w_N^{-q k}
       }
       cl_wait();                                   // peers are done with their scatter buffers
@@ -849,8 +983,8 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #pragma unroll
         for (int q = 0; q < C; ++q) st_async_cluster(mapa(xo, (uint32_t)q), z[p][q], mapa(xb, (uint32_t)q));
       }
-      mbar_wait_cta(xfull, (uint32_t)(it & 1));    // all C peers' scatters landed here
-      if (t == 0) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
+      if (!kNoPush) mbar_wait_cta(xfull, (uint32_t)(it & 1));    // all C peers' scatters landed here
+      if (t == 0 && !kNoPush) mbar_expect_tx(xfull, Cf::STAGE_BYTES);
       auto st = [&](int w, int j, float2* x) {
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
@@ -869,7 +1003,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     } else if constexpr (VEC) {
-      if constexpr (BS) mbar_wait_cta(yfull, (uint32_t)(it & 1));
+      if constexpr (BS && !SSR) mbar_wait_cta(yfull, (uint32_t)(it & 1));
 #pragma unroll
       for (int p = 0; p < PT; p += 2) {
         const int w = slot_w(p), k = slot_k(p);
@@ -885,7 +1019,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     } else {
-      if constexpr (BS) mbar_wait_cta(yfull, (uint32_t)(it & 1));
+      if constexpr (BS && !SSR) mbar_wait_cta(yfull, (uint32_t)(it & 1));
 #pragma unroll
       for (int p = 0; p < PT; ++p) {
         const int w = slot_w(p), k = slot_k(p);
@@ -897,19 +1031,31 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     }
-    if constexpr (MODE == AZ_TAIL) {              // flush this panel's candidates
+    if constexpr (MODE == AZ_TAIL || MODE == AZ_TAIL_SS) {   // flush this panel's candidates (+ list entries)
       if (a.rule == RULE_K) {
         __syncthreads();
         const uint32_t nc = min(tc.scount[0], (uint32_t)Cf::CAND_SMEM);
-        if (t == 0) misc[32] = nc ? atomicAdd(&a.st->cand_count, nc) : 0u;
+        uint32_t nl = 0;
+        if constexpr (MODE == AZ_TAIL_SS) nl = min(tc.scount[2], (uint32_t)kSlCap);
+        if (t == 0) {
+          misc[32] = nc ? atomicAdd(&a.st->cand_count, nc) : 0u;
+          if constexpr (MODE == AZ_TAIL_SS) misc[34] = nl ? atomicAdd(&tc.wcnt[panel], nl) : 0u;
+        }
         __syncthreads();
         const uint32_t b0 = misc[32];
         for (uint32_t i = t; i < nc; i += T) {
           const uint32_t g = b0 + i;
           if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
         }
+        if constexpr (MODE == AZ_TAIL_SS) {
+          SsEntry* dst = tc.went + (size_t)panel * tc.capp + misc[34];
+          for (uint32_t i = t; i < nl; i += T) dst[i] = tc.sl_buf[i];
+        }
         __syncthreads();
-        if (t == 0) tc.scount[0] = 0u;
+        if (t == 0) {
+          tc.scount[0] = 0u;
+          tc.scount[2] = 0u;
+        }
       }
     }
     if constexpr (PP && BS) {
@@ -923,6 +1069,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     }
   }
 
+  pdl_launch_dependents();                         // last panel done: the next kernel may start
   if (it > 0) cl_wait();                           // pairs with the last arrive
   if constexpr (DEFER) {
     if (it > 0) defer_finish(cid + (it - 1) * ncl, it - 1);   // the last panel (its arrive is unpaired:
@@ -943,7 +1090,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     }
     Ops::red_commit_mode(a, u, misc + 33);
   }
-  if constexpr (MODE == AZ_TAIL) {
+  if constexpr (MODE == AZ_TAIL || MODE == AZ_TAIL_SS) {
     __syncthreads();
     if (a.rule == RULE_K) {
       for (int i = t; i < HIST_BINS; i += T) {
@@ -997,14 +1144,25 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   CUtensorMap tm;
   // the head sweep's panel loads: 64-byte L2 promotion (measured 0.391 -> 0.381 ms at c3; the
   // other sweeps are fastest with the default 256 B)
+#if !defined(CSSAR_AZ_PROMO_RESID)
+#define CSSAR_AZ_PROMO_RESID -1
+#endif
+#if !defined(CSSAR_AZ_PROMO_TAIL)
+#define CSSAR_AZ_PROMO_TAIL -1
+#endif
+#if !defined(CSSAR_AZ_PROMO_Y)
+#define CSSAR_AZ_PROMO_Y -1
+#endif
   e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM,
-                                     MODE == AZ_FWD_THR ? (int)CU_TENSOR_MAP_L2_PROMOTION_L2_64B : -1);
+                         MODE == AZ_FWD_THR ? (int)CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         : MODE == AZ_RESID ? CSSAR_AZ_PROMO_RESID
+                         : az_is_tail(MODE) ? CSSAR_AZ_PROMO_TAIL : -1);
   if (e != cudaSuccess) return e;
   CUtensorMap tmy = tm;
   if constexpr (MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b with
     // consecutive rows ({col, 0, row}), box {W, 1, min(M/C, 256)}
     e = make_az_tensor_map(&tmy, MODE == AZ_RESID ? (const void*)a.Y : (const void*)a.b, n_rg, 1 << LOGN, 1, Cf::W,
-                           Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256, -1);
+                           Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256, CSSAR_AZ_PROMO_Y);
     if (e != cudaSuccess) return e;
   }
   const int npan = n_rg / Cf::W;
@@ -1017,15 +1175,25 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   cfg.blockDim = dim3(Cf::T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = Cf::C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
-  attr[1].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)policy;
+  cudaLaunchAttribute attr[3];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = Cf::C;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (policy) {
+    attr[na].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[na].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)policy;
+    ++na;
+  }
+  if (pdl_enabled()) {                           // programmatic dependent launch (cluster.cuh)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = policy ? 2 : 1;
+  cfg.numAttrs = na;
   e = cudaLaunchKernelEx(&cfg, k, a, tm, tmy);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -1097,6 +1265,16 @@ cudaError_t az_dispatch_mode(int mode, int n_rg, const AzArgs& a, cudaStream_t s
     case AZ_TAIL: return az_launch<LOGN, AZ_TAIL>(n_rg, a, s);
     case AZ_GRAD: return az_launch<LOGN, AZ_GRAD>(n_rg, a, s);
     case AZ_NORM: return az_launch<LOGN, AZ_NORM>(n_rg, a, s);
+    case AZ_FWD_SS:
+    case AZ_TAIL_SS:
+    case AZ_TAIL_SSD:
+      if constexpr (AzShape<LOGN, false>::C > 1) {
+        return mode == AZ_FWD_SS ? az_launch<LOGN, AZ_FWD_SS>(n_rg, a, s)
+             : mode == AZ_TAIL_SS ? az_launch<LOGN, AZ_TAIL_SS>(n_rg, a, s)
+                                  : az_launch<LOGN, AZ_TAIL_SSD>(n_rg, a, s);
+      } else {
+        return cudaErrorInvalidValue;              // sparse state: cluster sweeps only (n_az >= 2048)
+      }
     default: return cudaErrorInvalidValue;
   }
 }

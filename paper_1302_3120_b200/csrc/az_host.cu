@@ -10,6 +10,11 @@
 
 namespace cssar {
 
+bool pdl_enabled() {
+  static const bool on = [] { const char* v = std::getenv("CSSAR_PDL"); return v && std::atoi(v) != 0; }();
+  return on;
+}
+
 std::mutex& az_setup_mutex() {
   static std::mutex m;
   return m;

@@ -58,6 +58,13 @@ CSSAR_DEV void mbar_wait(const uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): kernels of the ITA loop are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so the next kernel's CTAs can start (SMEM
+// tables, mbarrier set-up) while this one drains; pdl_wait() blocks until the previous kernel
+// has completed and its memory is visible (a no-op without the attribute).
+CSSAR_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+CSSAR_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 CSSAR_DEV uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));

@@ -56,10 +56,11 @@ CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
     f = (2.0f / 3.0f) * (1.0f + cosf(2.09439510239319549f - (2.0f / 3.0f) * phi));
     f = sigma == 0.f ? 1.0f : f;
   }
-  f = (u > s2bits) ? f : 0.0f;                             // strict survival on the |b|^2 pattern
-  // explicitly rounded product: an FMA contraction with the consumer (e.g. the first FFT
+  // strict survival on the |b|^2 pattern; a removed entry is +0 (not b * 0, whose sign would
+  // follow b: the sparse-state schedule's zero-filled X must equal the dense one bitwise).
+  // Explicitly rounded products: an FMA contraction with the consumer (e.g. the first FFT
   // butterfly) would make E(b) inside a kernel round differently from the X it returns
-  return make_float2(__fmul_rn(b.x, f), __fmul_rn(b.y, f));
+  return (u > s2bits) ? make_float2(__fmul_rn(b.x, f), __fmul_rn(b.y, f)) : make_float2(0.0f, 0.0f);
 }
 
 CSSAR_DEV uint32_t mask_bit(const uint32_t* mask, int words, int row, int col) {

@@ -171,6 +171,9 @@ struct Engine {
   template <int LR, int LNS, int DIR>
   static CSSAR_DEV void butterflies(float2 (&v)[E], int t, const float2* tw) {
     constexpr int R = 1 << LR, NS = 1 << LNS, L = NS * R;
+#if defined(CSSAR_EXP_NOFFT_AZ)
+    if constexpr (BMINOR) return;       // experiment: azimuth data movement without the arithmetic
+#endif
 #pragma unroll
     for (int m = 0; m < E / R; ++m) {
       int b, j;
@@ -250,8 +253,17 @@ struct Engine {
     butterflies<LR, LNS, DIR>(v, t, tw + tw_off<REV>(p));
     if constexpr (p + 1 < P) {
       __syncthreads();                 // everyone finished reading the previous exchange
+#if defined(CSSAR_EXP_NOXCH_AZ)
+      if constexpr (!BMINOR) {         // experiment: azimuth passes without the SMEM exchange
+#endif
       write<LR, LNS>(s, v, t);
+#if defined(CSSAR_EXP_NOXCH_AZ)
+      }
+#endif
       __syncthreads();
+#if defined(CSSAR_EXP_NOXCH_AZ)
+      if constexpr (!BMINOR)
+#endif
       read<lr<REV>(p + 1), LR, LNS>(s, v, t);
       passes_from<DIR, REV, p + 1>(s, v, t, tw);
     }

@@ -1,6 +1,7 @@
 // Kernel declarations and device-side shared structures for libcssar.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include "common.cuh"
 
@@ -52,9 +53,25 @@ struct SelState {
   double mu_den;            // ||Theta G(dX_k)||^2 (AZ_NORM)
   float mu;                 // mu_i of the current iteration (adaptive runs), else 0
   float lambda;             // fixed-lambda rule: lambda (adaptive runs recompute sigma = f(lambda mu_i))
+  // sparse-state schedule: counters of the list the next S5 writes are zeroed by the select;
+  // ss_fell records that this iteration's select needed the dense fallback (list rebuild)
+  uint32_t* ss_cnt[2];
+  int32_t ss_npan;
+  int32_t ss_fell;
 };
 
 struct IterLogDev { float sigma; float lam; long long support; double resid2; float mu; float gap; int gap_exact; };
+
+// sparse-state schedule (NEXT-3): one list entry: b at (row, column col0 + w of the panel)
+struct SsEntry { uint32_t row; uint32_t w; float2 v; };
+// the two state lists (iteration parity): panel p's entries at ent[l][p * capp ...], count cnt[l][p]
+struct SsLists {
+  SsEntry* ent[2];
+  uint32_t* cnt[2];
+  uint32_t capp;            // entries per panel (= n_az * W: a panel never overflows)
+  int npan;
+  int W;
+};
 
 struct AzArgs {
   const float2* in;
@@ -87,6 +104,7 @@ struct AzArgs {
   // arrays [3][kRedSlots] reduced in block order by the last CTA (ticket counter per mode)
   double* red_part;
   uint32_t* red_ticket;
+  SsLists ss;               // sparse-state modes
 };
 constexpr int kRedSlots = 8192;   // >= the grid of every reducing azimuth launch
 
@@ -130,7 +148,34 @@ enum AzMode : int {
   AZ_TAIL = 6,        // b <- E(b; sigma) + mu F_eta^-1 u, histogram  (S5)
   AZ_GRAD = 7,        // adaptive step: dX = F_eta^-1 u -> D; F_eta (dX on supp X_i); ||dX_k||^2
   AZ_NORM = 8,        // adaptive step: ||Theta o F_eta^-1 u||^2 only
+  // sparse-state schedule (NEXT-3; world 1, k-rule): the state is a per-panel list of the b
+  // entries above the candidate window's floor instead of a dense b array
+  AZ_FWD_SS = 9,      // S1: X = E(b; sigma) from the list, scattered into the stage; F_eta
+  AZ_TAIL_SS = 10,    // S5: X_i from the list; b_i = X_i + mu dX -> histogram, candidates, new list
+  AZ_TAIL_SSD = 11,   // S5 re-run after a select fallback: dense b_i into a.b (early exit otherwise)
 };
+constexpr bool az_is_thr(int m) { return m == AZ_FWD_THR || m == AZ_FWD_SS; }
+constexpr bool az_is_tail(int m) { return m == AZ_TAIL || m == AZ_TAIL_SS || m == AZ_TAIL_SSD; }
+constexpr bool az_is_ss(int m) { return m == AZ_FWD_SS || m == AZ_TAIL_SS || m == AZ_TAIL_SSD; }
+
+
+// programmatic dependent launch of the ITA-loop kernels (opt-in: CSSAR_PDL=1; measured neutral
+// in the replayed graph at c3)
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // host-side launchers (kernels.cu)
 cudaError_t launch_rg_sweep(int log_nrg, bool gbody, int n_rows, const RgArgs& a, cudaStream_t s);   // blocked iff a.blk != 0
@@ -138,6 +183,10 @@ cudaError_t launch_az(int log_naz, int mode, int n_rg_local, const AzArgs& a, cu
 cudaError_t launch_select(int n_threads_hint, float2* b, long long n, long long k, int rule, int thr, float mu,
                           SelState* st, uint32_t* hist, uint32_t* hist_full, uint32_t* cand, uint32_t cand_cap,
                           IterLogDev* log, int log_cap, cudaStream_t s);
+// the k-rule select after sel_coarse (fallback kernels + fine select)
+cudaError_t launch_select_rest(int sm_count, float2* b, long long n, long long k, int thr, float mu, SelState* st,
+                               uint32_t* hist, uint32_t* hist_full, uint32_t* cand, uint32_t cand_cap, IterLogDev* log,
+                               int log_cap, cudaStream_t s);
 // multi-GPU k-rule select, split around the all-reduces; world == 1 uses launch_select
 enum SelPart : int {
   SEL_COARSE = 0,     // global |b|^2 histogram (+ flags) -> target bin or fallback decision
@@ -185,6 +234,14 @@ cudaError_t launch_group_sum(int dtype, void* const* bufs, int world, long long 
 cudaError_t launch_init_state(SelState* st, uint32_t* hist, uint32_t* hist_full, int thr, float sigma_fixed,
                               cudaStream_t s);
 cudaError_t launch_finalize(float2* b, long long n, int thr, const SelState* st, cudaStream_t s);
+// sparse-state schedule (ss.cu): rebuild the list S1 reads next from the dense b of a fallback
+// iteration (force = always, e.g. after the dense iteration 0); X = E(b; sigma) from the last list
+cudaError_t launch_ss_rebuild(const float2* b, int n_az, int n_rg, const SsLists& L, const SelState* st, int force,
+                              cudaStream_t s);
+cudaError_t launch_ss_finalize(float2* X, int n_az, int n_rg, const SsLists& L, int thr, const SelState* st,
+                               cudaStream_t s);
+int az_panel_width(int log_naz);       // W of the head/tail cluster sweeps (0: not a cluster shape)
+cudaError_t launch_ss_set(SelState* st, uint32_t* cnt0, uint32_t* cnt1, int npan, cudaStream_t s);
 // precomputed SMEM tables (filled once per plan, copied into SMEM by each CTA)
 size_t rg_table_count(int log_nrg);
 int rg_rows_per_cta(int log_nrg);

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
       return (size_t)rr * N + j;
     }
   };
+  pdl_wait();                                 // the previous sweep's output is complete
   for (; row0 < nrows; row0 += (int)gridDim.x * C::B) {
   En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // raw row loads
 #pragma unroll
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
     for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
   });
   }
+  pdl_launch_dependents();                   // (at the end: dependents may not run ahead)
   if constexpr (BLK) {
     if (a.dst[0]) __threadfence_system();   // peer stores performed before the flag barrier
   }
@@ -344,7 +346,8 @@ static cudaError_t rg_launch(int n_rows, const RgArgs& a, cudaStream_t s) {
       b.nrows = n_rows;
     }
   }
-  k<<<grid, C::T, C::SMEM, s>>>(b);
+  e = launch_pdl(k, dim3(grid), dim3(C::T), C::SMEM, s, b);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -105,6 +105,7 @@ CSSAR_DEV void find_rank_bin(const uint32_t* cnt, const uint32_t* above, unsigne
 }
 
 __global__ void __launch_bounds__(1024) sel_coarse_kernel(long long k, SelState* st, const uint32_t* hist) {
+  pdl_wait();
   __shared__ uint32_t cnt[HIST_BINS], above[HIST_BINS], wt[32];
   __shared__ int sb;
   __shared__ uint32_t sr, sa;
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(1024) sel_coarse_kernel(long long k, SelState*
 
 __global__ void __launch_bounds__(512) fb_hist_kernel(const float2* __restrict__ b, long long n, const SelState* st,
                                                       uint32_t* hist_full) {
+  pdl_wait();
   if (!st->need_full) return;
   __shared__ uint32_t sh[HIST_BINS];
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) sh[i] = 0u;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(512) fb_hist_kernel(const float2* __restrict__
 }
 
 __global__ void __launch_bounds__(1024) fb_find_kernel(long long k, SelState* st, const uint32_t* hist_full) {
+  pdl_wait();
   if (!st->need_full) return;
   __shared__ uint32_t cnt[HIST_BINS], above[HIST_BINS], wt[32];
   __shared__ int sb;
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(1024) fb_find_kernel(long long k, SelState* st
 
 __global__ void __launch_bounds__(512) fb_collect_kernel(const float2* __restrict__ b, long long n, SelState* st,
                                                          uint32_t* cand, uint32_t cap) {
+  pdl_wait();
   if (!st->need_full) return;
   const int B = st->target_bin;
   __shared__ uint32_t buf[2048];
@@ -253,8 +257,17 @@ CSSAR_DEV void finish_select(uint32_t s2, unsigned long long abv, int thr, float
     hist[i] = 0u;
     if (nf && i < HIST_BINS) hist_full[i] = 0u;
   }
+  // sparse-state schedule: the list the next S5 writes starts empty (it was last read by this
+  // iteration's S1 / S5)
+  if (st->ss_cnt[0]) {
+    uint32_t* c = st->ss_cnt[st->iter & 1];
+    for (int i = t; i < st->ss_npan; i += blockDim.x) c[i] = 0u;
+  }
   __syncthreads();
-  if (t == 0) st->need_full = 0;
+  if (t == 0) {
+    st->ss_fell = nf;          // a fallback iteration: ss_rebuild re-derives the list from dense b
+    st->need_full = 0;
+  }
 }
 
 // one 10-bit radix level: counts of (u >> sh) & 1023 among the |b|^2 patterns u with
@@ -316,6 +329,7 @@ __global__ void __launch_bounds__(1024) sel_fine_kernel(long long k, int thr, fl
                                                         uint32_t* hist, uint32_t* hist_full, const uint32_t* cand,
                                                         uint32_t cap, IterLogDev* log, int log_cap, const float2* b,
                                                         long long n) {
+  pdl_wait();
   __shared__ uint32_t cnt[1024], above[1024], wt[32];
   __shared__ int sd;
   __shared__ uint32_t sr, sa, smin;
@@ -459,12 +473,27 @@ cudaError_t launch_select(int sm_count, float2* b, long long n, long long k, int
     lambda_step_kernel<<<1, 1, 0, s>>>(st, thr, mu, log, log_cap);
     return cudaGetLastError();
   }
+  cudaError_t e = launch_pdl(sel_coarse_kernel, dim3(1), dim3(1024), 0, s, k, st, (const uint32_t*)hist);
+  if (e != cudaSuccess) return e;
+  return launch_select_rest(sm_count, b, n, k, thr, mu, st, hist, hist_full, cand, cand_cap, log, log_cap, s);
+}
+
+cudaError_t launch_select_rest(int sm_count, float2* b, long long n, long long k, int thr, float mu, SelState* st,
+                               uint32_t* hist, uint32_t* hist_full, uint32_t* cand, uint32_t cand_cap, IterLogDev* log,
+                               int log_cap, cudaStream_t s) {
   const int grid = sm_count * 4;
-  sel_coarse_kernel<<<1, 1024, 0, s>>>(k, st, hist);
-  fb_hist_kernel<<<grid, 512, 0, s>>>(b, n, st, hist_full);
-  fb_find_kernel<<<1, 1024, 0, s>>>(k, st, hist_full);
-  fb_collect_kernel<<<grid, 512, 0, s>>>(b, n, st, cand, cand_cap);
-  sel_fine_kernel<<<1, 1024, 0, s>>>(k, thr, mu, st, hist, hist_full, cand, cand_cap, log, log_cap, b, n);
+  cudaError_t e;
+  if ((e = launch_pdl(fb_hist_kernel, dim3(grid), dim3(512), 0, s, (const float2*)b, n, (const SelState*)st,
+                      hist_full)) != cudaSuccess)
+    return e;
+  if ((e = launch_pdl(fb_find_kernel, dim3(1), dim3(1024), 0, s, k, st, (const uint32_t*)hist_full)) != cudaSuccess)
+    return e;
+  if ((e = launch_pdl(fb_collect_kernel, dim3(grid), dim3(512), 0, s, (const float2*)b, n, st, cand, cand_cap)) !=
+      cudaSuccess)
+    return e;
+  if ((e = launch_pdl(sel_fine_kernel, dim3(1), dim3(1024), 0, s, k, thr, mu, st, hist, hist_full,
+                      (const uint32_t*)cand, cand_cap, log, log_cap, (const float2*)b, n)) != cudaSuccess)
+    return e;
   return cudaGetLastError();
 }
 

@@ -77,16 +77,18 @@ def _teacher_forced(prob, op, pl, Xin_c64, k):
 
 
 # ------------------------------------------------------------------------------------ c3
-def test_c3_full_run_vs_oracle_trajectory():
+@pytest.mark.parametrize("sparse_state", [False, True])
+def test_c3_full_run_vs_oracle_trajectory(sparse_state):
     """c3's full 100 iterations on the GPU vs the oracle's X_100 (rel-L2 <= 1e-3), all 500
-    bright targets (|sigma| = 10) in both supports, sigma and support logs at every iteration."""
+    bright targets (|sigma| = 10) in both supports, sigma and support logs at every iteration;
+    dense-b and sparse-state (NEXT-3) schedules."""
     g = _golden()
     prob = problem("c3")
     cfg = prob.cfg
     assert int(g["k"]) == cfg.k and int(g["iters"]) == cfg.iters == 100
     pl = _plan(cfg.params)
     Xg, glog = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr="soft", rule="k", k=cfg.k,
-                              iters=cfg.iters, log=True)
+                              iters=cfg.iters, log=True, sparse_state=sparse_state)
     Xg = to_host(Xg)
     Xo = _dense(Xg.shape, g["X100_idx"], g["X100_val"])
     err = rel_l2(Xg, Xo)

@@ -24,8 +24,8 @@ def main():
     pl = Plan(SarParams(n_az=n_az, n_rg=n_rg), op=op)
     k = n_az * n_rg // 100
     X = torch.zeros_like(Y)
-    pl.ita_iterate(Y, mb, X=X, k=k, iters=3)
-    pl.ita_iterate(Y, mb, X=X, k=k, iters=iters, profile_stages=True)
+    pl.ita_iterate(Y, mb, X=X, k=k, iters=3, check=False)
+    pl.ita_iterate(Y, mb, X=X, k=k, iters=iters, profile_stages=True, check=False)
     st, it = pl.stage_times()
     print(json.dumps({"grid": [n_az, n_rg], "op": op, **{kk: round(v / it, 4) for kk, v in st.items()}}))
 
