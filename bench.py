@@ -3,12 +3,13 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl cssar|reference]
 
-Workload (BASELINE.json configs[3], the largest scene the metric's 1..8-GPU runs use that
-fits one GPU): c3, 8192 x 8192 complex64, 1% Rayleigh clutter + 500 bright targets, 60%
-azimuth-line mask, 15 dB, soft threshold, k-rule k = 671589, mu = 1.  Synthetic inputs
-from inputs/ (seeded), echo Y = Theta o (G(X_true) + noise) generated with the library's
-own forward operator (P:L47 inverse-focusing simulation); arrays are 512 MiB each, larger
-than L2 (126 MB), so no L2 flush is needed between steps.
+Workload: BASELINE.json configs[3] (c3), the configuration the metric's 1/2/4/8-GPU runs are
+quoted on: 8192 x 8192 complex64, 1% Rayleigh clutter + 500 bright targets, 60% azimuth-line
+mask, 15 dB, soft threshold, k-rule k = 671589, mu = 1.  (c4, 32768 x 16384, also fits one
+B200; it is measured in the line's "c4" object.)  Synthetic inputs from inputs/ (seeded), echo
+Y = Theta o (G(X_true) + noise) generated with the library's own forward operator (P:L47
+inverse-focusing simulation); arrays are 512 MiB each, larger than L2 (126 MB), so no L2
+flush is needed between steps.
 
 Prints ONE JSON line (rank 0).  value = complex samples * iterations / s of the scene.
 N > 1 (torchrun): the SAME c3 scene slab-partitioned over the ranks by azimuth lines
@@ -48,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the c4 (32768 x 16384) object")
+    ap.add_argument("--no-sparse-state", action="store_true", help="skip the sparse-state (NEXT-3) object")
     ap.add_argument("--peer-transpose", action="store_true",
                     help="N > 1: fused peer-memory transposes and the sparse-X' sweep (not yet validated on >1 GPU)")
     return ap.parse_args()
@@ -120,6 +123,80 @@ def make_problem_gpu(cfg, plan, seed_offset=0):
     del Yc, noise, X
     torch.cuda.synchronize()
     return Y.contiguous(), mb, mask, sc
+
+
+def timed_iters(plan, Y, mb, X, iters, **kw):
+    """Device time (CUDA events on the current stream) of one ita_iterate call of `iters`."""
+    import torch
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    plan.ita_iterate(Y, mb, X=X, iters=iters, check=False, **kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    plan.status()
+    return e0.elapsed_time(e1)
+
+
+def stage_profile(plan, Y, mb, X, iters, **kw):
+    plan.ita_iterate(Y, mb, X=X, iters=iters, profile_stages=True, **kw)
+    st_ms, it_meas = plan.stage_times()
+    return {k: v / it_meas for k, v in st_ms.items()}
+
+
+def measure_c4(args, peak, peak_kind):
+    """BASELINE.json configs[4] (c4, 32768 x 16384, Fr = 120 MHz, 0.5% clutter, 50% mask,
+    k = 2684355, 50 iterations) on one GPU: graph-replayed iterations, per-step stage times,
+    the iteration's HBM roofline, and an end-to-end solve through the public API."""
+    import torch
+    from inputs import configs
+    from paper_1302_3120_b200 import Plan
+    from paper_1302_3120_b200.cssar import STAGES
+    cfg = configs.get("c4")
+    p = cfg.params
+    n = p.n_az * p.n_rg
+    plan = Plan(p)
+    Y, mb, mask, sc = make_problem_gpu(cfg, plan)
+    del mask
+    X = torch.zeros_like(Y)
+    kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
+    plan.ita_iterate(Y, mb, X=X, iters=3, **kw)
+    steps = 10
+    ms = timed_iters(plan, Y, mb, X, steps, **kw)
+    it_s = steps / (ms * 1e-3)
+    stages = stage_profile(plan, Y, mb, X, 5, **kw)
+    dom = max((s for s in STAGES if s != "S6_select"), key=lambda s: stages[s])
+    dom_ach = BYTES_PER_SAMPLE[dom] * n / (stages[dom] * 1e-3) / 1e9
+    iter_ach = ITER_BYTES_PER_SAMPLE * n * it_s / 1e9
+    out = {"workload": f"c4: {p.n_az}x{p.n_rg} complex64, Fr {p.Fr / 1e6:.0f} MHz, {cfg.scene} scene, {cfg.mask} "
+                       f"mask {cfg.rate}, SNR {cfg.snr_db} dB, soft threshold, k = {cfg.k}",
+           "value": n * it_s, "unit": "samples*it/s", "ms_per_step": ms / steps, "it_per_s": it_s, "steps": steps,
+           "stages_ms": stages,
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak, "unit": "GB/s",
+                        "frac": dom_ach / peak, "peak_kind": peak_kind,
+                        "algorithmic_bytes_per_launch": BYTES_PER_SAMPLE[dom] * n, "avg_launch_ms": stages[dom]},
+           "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak, "unit": "GB/s",
+                                  "frac": iter_ach / peak, "bytes_per_sample": ITER_BYTES_PER_SAMPLE},
+           "select_fallbacks": plan.debug_fallbacks()}
+    if not args.no_e2e:
+        Yh = Y.cpu().pin_memory()
+        mbh = mb.cpu().pin_memory()
+        del Y, X
+        torch.cuda.empty_cache()
+        Xh = torch.empty_like(Yh).pin_memory()
+        plan.solve_host(Yh, mbh, out_host=Xh, iters=2, **kw)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.solve_host(Yh, mbh, out_host=Xh, iters=cfg.iters, **kw)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["e2e"] = {"value": n * cfg.iters / dt, "unit": "samples*it/s",
+                      "h2d_bytes_per_step": (Yh.numel() * 8 + mbh.numel() * 4) / cfg.iters,
+                      "d2h_bytes_per_step": Xh.numel() * 8 / cfg.iters, "solve_iters": cfg.iters}
+    del plan
+    torch.cuda.empty_cache()
+    return out
 
 
 def cpu_baseline(cfg_name, n_az, n_rg, iters):
@@ -319,8 +396,24 @@ def main():
         line["e2e"] = {"value": n * iters / dt, "unit": "samples*it/s", "h2d_bytes_per_step": h2d / iters,
                        "d2h_bytes_per_step": d2h / iters, "solve_iters": iters,
                        "note": "one full reconstruction (config iteration count) per call; copies once per solve"}
+    if world == 1 and not args.no_sparse_state and cfg.rule == "k":
+        # NEXT-3 sparse-state schedule (CSSAR_FLAG_SPARSE_STATE) on the same workload: 72.125
+        # algorithmic HBM B/sample instead of 96.125 (the dense b traffic of S1 and S5 removed)
+        plan.ita_iterate(Y, mb, X=X, iters=max(3, args.warmup), sparse_state=True, **kw)
+        ms_ss = timed_iters(plan, Y, mb, X, args.steps, sparse_state=True, **kw)
+        st_ss = stage_profile(plan, Y, mb, X, 10, sparse_state=True, **kw)
+        it_ss = args.steps / (ms_ss * 1e-3)
+        line["sparse_state"] = {"ms_per_step": ms_ss / args.steps, "it_per_s": it_ss, "value": n * it_ss,
+                                "unit": "samples*it/s", "bytes_per_sample": 72.125,
+                                "iteration_achieved_GBps": 72.125 * n * it_ss / 1e9, "stages_ms": st_ss,
+                                "note": "opt-in schedule; bitwise the dense schedule's results"}
+    if world == 1 and not args.no_c4 and args.config == "c3":
+        del Y, X
+        torch.cuda.empty_cache()
+        line["c4"] = measure_c4(args, peak, peak_kind)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, 4096, 4096, 2)
+        # the oracle on the full c3 grid (one ITA iteration; ~10-30 s of host work)
+        line["cpu_baseline"] = cpu_baseline(args.config, p.n_az, p.n_rg, 1)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

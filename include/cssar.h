@@ -85,7 +85,7 @@ typedef enum { CSSAR_RULE_KSPARSE = 1 /* P:L320 */, CSSAR_RULE_FIXED_LAMBDA = 2 
  * events between the six steps S1..S6 on `stream`, synchronising once per iteration, and
  * accumulates per-step device time (read with cssar_stage_times). */
 enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPARSE_X = 4,
-       CSSAR_FLAG_PEER_TRANSPOSE = 8, CSSAR_FLAG_SPARSE_STATE = 16 };
+       CSSAR_FLAG_PEER_TRANSPOSE = 8, CSSAR_FLAG_SPARSE_STATE = 16, CSSAR_FLAG_FUSE_LAMBDA = 32 };
 
 /* ITA settings (Algorithm 1 "Initial": lambda, mu, I_max).  iters = number of X updates
  * (R18).  k is used by the k-rule, lambda by the fixed-lambda rule.
@@ -107,6 +107,13 @@ enum { CSSAR_FLAG_PROFILE_STAGES = 1, CSSAR_FLAG_ADAPTIVE_MU = 2, CSSAR_FLAG_SPA
  * iteration).  A select fallback re-runs S5 densely into X_inout.  Same results as the dense
  * schedule (bitwise).  Not the default: the sweeps are latency-bound, and on B200 the list
  * fills cost more than the dense b traffic they save.
+ * CSSAR_FLAG_FUSE_LAMBDA (a request; fixed-lambda rule -- eq. 7: sigma = lambda mu is known
+ * before the iteration's select -- fixed mu, tol = 0, world 1): S5 is fused with the next
+ * iteration's S1 -- one azimuth sweep computes b_i = E(b_(i-1)) + mu dX, stores it and
+ * transforms X_(i+1) = E(b_i; sigma) for the next G body (88.125 instead of 96.125 B/sample,
+ * one sweep fewer).  Equal to the unfused schedule up to floating-point order (another FFT
+ * factorisation).  Not the default: the fused sweep has the residual sweep's two cluster
+ * exchanges and measured slower at c3 (2.47 vs 2.39 ms per iteration).
  * CSSAR_FLAG_PEER_TRANSPOSE (world > 1; a request): the fused transposes -- sweep epilogues
  * store straight into the peers' slabs through the CUDA-IPC mappings made at bind time, a
  * device flag barrier (system-scope release/acquire on slots in every rank's workspace, 20 s

@@ -356,8 +356,10 @@ cudaError_t launch_select_ss(cssar_plan pl, AzArgs a, float2* b, const cssar_ita
 }
 
 // one ITA iteration (S1..S6) on stream s
+// fuse: fixed-lambda schedule -- S5 fused with the next iteration's S1 (AZ_FUSE); the iteration
+// runs S1 only when s1 is set (the first one)
 int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const cssar_ita_params& prm, void* X,
-                      cudaStream_t s, bool prof = false, bool ss = false) {
+                      cudaStream_t s, bool prof = false, bool ss = false, bool fuse = false, bool s1 = true) {
   // PROFILE_STAGES: CUDA events between the steps, and NVTX ranges S1..S6 for nsys timelines
   static const char* const kStage[6] = {"S1 az head", "S2 range G", "S3 az residual", "S4 range M", "S5 az tail",
                                          "S6 select"};
@@ -395,7 +397,7 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
   // S1: X_i = E(b_{i-1}; sigma_{i-1}); F_eta   (sparse state: b_{i-1} from the list)
   a.in = ss ? pl->U : b;                 // (FWD_SS reads no dense input; any mapped pointer)
   a.out = pl->U;
-  CUDA_TRY(launch_az(pl->log_naz, ss ? AZ_FWD_SS : AZ_FWD_THR, a.n_rg, a, s));
+  if (s1) CUDA_TRY(launch_az(pl->log_naz, ss ? AZ_FWD_SS : AZ_FWD_THR, a.n_rg, a, s));
   MARK(1);
   // S2: G body
   CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
@@ -424,6 +426,13 @@ int enqueue_iteration(cssar_plan pl, const void* Y, const uint32_t* mask, const 
     CUDA_TRY(launch_rg_sweep(pl->log_nrg, true, (int)pl->p.n_az, r, s));
     CUDA_TRY(launch_az(pl->log_naz, AZ_NORM, a.n_rg, a, s));
     CUDA_TRY(launch_adaptive_step(a, pl->n, pl->sm_count, s));
+  } else if (fuse) {
+    // S5 + next S1 (fixed lambda): b_i stored, X_{i+1} = E(b_i; sigma) transformed into U
+    a.in = pl->U;
+    a.out = pl->U;
+    a.tw = pl->d_az_tab_r;
+    CUDA_TRY(launch_az(pl->log_naz, AZ_FUSE, a.n_rg, a, s));
+    a.tw = pl->d_az_tab;
   } else if (ss) {
     // S5 (sparse state): X_i from the list; b_i -> histogram, candidates and the next list
     a.in = pl->U;
@@ -1427,6 +1436,10 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   // stop, cluster azimuth shapes; iteration 0 (arbitrary X_0) runs dense and its b_0 seeds the list
   const bool ss = pl->ss_ok && prm->rule == CSSAR_RULE_KSPARSE && !(prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && !tol &&
                   (prm->flags & CSSAR_FLAG_SPARSE_STATE) && prm->iters >= 2;
+  // fixed-lambda fused schedule (CSSAR_FLAG_FUSE_LAMBDA: S5 + next S1 in one sweep, 88.125
+  // B/sample) for the fixed-lambda rule with a fixed step and no tolerance stop
+  const bool fuse = prm->rule == CSSAR_RULE_FIXED_LAMBDA && !(prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && !tol &&
+                    (prm->flags & CSSAR_FLAG_FUSE_LAMBDA);
   if (ss) {
     for (int l = 0; l < 2; ++l)
       CUDA_TRY(cudaMemsetAsync(pl->ss.cnt[l], 0, sizeof(uint32_t) * (size_t)pl->ss.npan, s));
@@ -1462,7 +1475,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
     for (int i = 0; i < 6; ++i) pl->stage_ms[i] = 0.0;
     pl->stage_iters = 0;
     for (int it = 0; it < prm->iters; ++it) {
-      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, true, ss && it > 0);
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, true, ss && it > 0, fuse, !fuse || it == 0);
       if (rc != CSSAR_OK) return rc;
       if (ss && it == 0 && (rc = ss_seed()) != CSSAR_OK) return rc;
       CUDA_TRY(cudaEventSynchronize(pl->ev[6]));
@@ -1484,15 +1497,22 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
       if (rc != CSSAR_OK) return rc;
       if ((rc = ss_seed()) != CSSAR_OK) return rc;
       first = 1;
+    } else if (fuse) {                         // iteration 0 with its S1, outside the graph
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, s, false, false, true, true);
+      if (rc != CSSAR_OK) return rc;
+      bool stop = false;
+      if ((rc = converged(0, stop)) != CSSAR_OK) return rc;
+      first = 1;
     }
     GraphKey key{Y, mask_bits, X_inout, prm->thr, prm->rule, prm->rule == CSSAR_RULE_KSPARSE ? prm->k : 0,
-                 prm->lambda, prm->mu, (prm->flags & CSSAR_FLAG_ADAPTIVE_MU) | (ss ? CSSAR_FLAG_SPARSE_STATE << 8 : 0)};
+                 prm->lambda, prm->mu,
+                 (prm->flags & CSSAR_FLAG_ADAPTIVE_MU) | (ss ? CSSAR_FLAG_SPARSE_STATE << 8 : 0) | (fuse ? 1 << 20 : 0)};
     if (!pl->ghave || !(pl->gkey == key)) {
       if (pl->gexec) { cudaGraphExecDestroy(pl->gexec); pl->gexec = nullptr; }
       pl->ghave = false;
       cudaGraph_t g = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
-      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, pl->cap_stream, false, ss);
+      int rc = enqueue_iteration(pl, Y, mask_bits, *prm, X_inout, pl->cap_stream, false, ss, fuse, !fuse);
       cudaError_t ec = cudaStreamEndCapture(pl->cap_stream, &g);
       if (rc != CSSAR_OK) { if (g) cudaGraphDestroy(g); return rc; }
       CUDA_TRY(ec);

@@ -182,7 +182,7 @@ template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR || MODE == AZ_FWD_SS) ? -1 : +1;   // first transform direction
   // kernels that reduce a squared norm into the solver state
-  static constexpr bool RED = MODE == AZ_RESID || MODE == AZ_GRAD || MODE == AZ_NORM;
+  static constexpr bool RED = az_is_res(MODE) || MODE == AZ_NORM;
   CSSAR_DEV static double* red_target(const AzArgs& a) {
     return MODE == AZ_RESID ? &a.st->resid2 : MODE == AZ_GRAD ? &a.st->mu_num : &a.st->mu_den;
   }
@@ -207,7 +207,7 @@ struct AzOps {
       x.v = __ldg(a.Y + idx);
     } else if constexpr (MODE == AZ_INV_MASK || MODE == AZ_NORM) {
       x.m = mask_word(a.mask, a.mask_words, row, col);
-    } else if constexpr (MODE == AZ_TAIL || MODE == AZ_GRAD) {
+    } else if constexpr (MODE == AZ_TAIL || MODE == AZ_GRAD || MODE == AZ_FUSE) {
       x.v = a.b[idx];
     }
     return x;
@@ -234,9 +234,22 @@ struct AzOps {
   }
 
   // RESID mid: g = G(X) sample; r = Theta o (Y - g).  GRAD mid (ax.v = b_{i-1}): dX = the
-  // sample, kept in D; returns dX on supp(X_i) = {|b_{i-1}|^2 > sigma_{i-1}^2} (R20)
-  CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc, int row, int col, uint32_t s2) {
-    if constexpr (MODE == AZ_GRAD) {
+  // sample, kept in D; returns dX on supp(X_i) = {|b_{i-1}|^2 > sigma_{i-1}^2} (R20).
+  // FUSE mid (ax.v = b_{i-1}): b_i = E(b_{i-1}; sigma_{i-1}) + mu dX stored; returns
+  // X_{i+1} = E(b_i; sigma_fixed) (eq. 7: sigma = lambda mu is known before the select) and
+  // counts its support in acc
+  CSSAR_DEV static float2 mid(const AzArgs& a, float2 x, const Aux& ax, float& acc, int row, int col, uint32_t s2,
+                              float sig = 0.f, uint32_t s2f = 0u, float sigf = 0.f) {
+    if constexpr (MODE == AZ_FUSE) {
+      const float2 dx = x * a.scale;
+      const float2 xk = threshold(ax.v, s2, sig, a.thr);
+      const float2 bn = make_float2(fmaf(a.mu, dx.x, xk.x), fmaf(a.mu, dx.y, xk.y));
+      a.b[(size_t)row * a.n_rg + col] = bn;
+      const uint32_t u = mag2_bits(bn);
+      if (u > s2f) acc += 1.0f;
+      if (u >= 0x7F800000u) a.st->nonfinite = 1u;
+      return threshold(bn, s2f, sigf, a.thr);
+    } else if constexpr (MODE == AZ_GRAD) {
       const float2 d = x * a.scale;
       a.D[(size_t)row * a.n_rg + col] = d;
       const float2 z = mag2_bits(ax.v) > s2 ? d : make_float2(0.f, 0.f);
@@ -327,10 +340,10 @@ struct AzOps {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>::T,
-                                  ((MODE == AZ_RESID || MODE == AZ_GRAD) && AzShape<LOGN, true>::MINB > 2) ? 2 : AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>::MINB)
+__global__ void __launch_bounds__(AzShape<LOGN, az_is_res(MODE)>::T,
+                                  ((az_is_res(MODE)) && AzShape<LOGN, true>::MINB > 2) ? 2 : AzShape<LOGN, az_is_res(MODE)>::MINB)
     az_kernel(const AzArgs a) {
-  using Cf = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>;
+  using Cf = AzShape<LOGN, az_is_res(MODE)>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E;
   constexpr int N = M * C;
   using En = typename Cf::En;
@@ -367,9 +380,15 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
 
   uint32_t s2 = 0u;
   float sig = 0.f;
-  if constexpr (MODE == AZ_FWD_THR || MODE == AZ_GRAD) {
+  uint32_t s2f = 0u;
+  float sigf = 0.f;
+  if constexpr (MODE == AZ_FWD_THR || MODE == AZ_GRAD || MODE == AZ_FUSE) {
     s2 = a.st->sigma2_bits;
     sig = a.st->sigma;
+  }
+  if constexpr (MODE == AZ_FUSE) {
+    s2f = a.st->sigma2_fixed_bits;
+    sigf = a.st->sigma_fixed;
   }
   // DIT-first input rows: local index m -> global row rank + C m; all loads of a group are
   // issued before the prologue arithmetic
@@ -385,7 +404,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
 
   static_assert(C == 1, "cluster shapes use az_cluster_kernel");
   {
-    if constexpr (MODE == AZ_RESID || MODE == AZ_GRAD) {
+    if constexpr (az_is_res(MODE)) {
       auto mid = [&](int w, int j, float2* x) {
         Aux ax[RL];
 #pragma unroll
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
           ax[r] = Ops::fetch(a, row, col0 + w, (size_t)row * n_rg + col0 + w);
         }
 #pragma unroll
-        for (int r = 0; r < RL; ++r) x[r] = Ops::mid(a, x[r], ax[r], racc, j + r * (M / RL), col0 + w, s2);
+        for (int r = 0; r < RL; ++r) x[r] = Ops::mid(a, x[r], ax[r], racc, j + r * (M / RL), col0 + w, s2, sig, s2f, sigf);
       };
       auto st = [&](int w, int j, float2* x) {
 #pragma unroll
@@ -422,6 +441,12 @@ __global__ void __launch_bounds__(AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_G
     }
   }
 
+  if constexpr (MODE == AZ_FUSE) {                 // support of X_{i+1} (integer-valued float counts)
+    unsigned long long cnt = (unsigned long long)racc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&a.st->support_fixed, cnt);
+  }
   if constexpr (Ops::RED) {
     // block reduce the squared norm -> one double atomic per CTA
     __shared__ float red[32];
@@ -575,7 +600,7 @@ template <int MODE>
 constexpr bool kAzDefer = az_is_thr(MODE);
 #endif
 template <int LOGN, int MODE>
-using AzClShape = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD, 0, az_is_tail(MODE), kAzDefer<MODE>,
+using AzClShape = AzShape<LOGN, az_is_res(MODE), 0, az_is_tail(MODE), kAzDefer<MODE>,
                           MODE == AZ_TAIL_SS>;
 
 template <int LOGN, int MODE>
@@ -585,7 +610,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   using Cf = AzClShape<LOGN, MODE>;
   constexpr int C = Cf::C, W = Cf::W, M = Cf::M, T = Cf::T, E = Cf::E, NS = Cf::NS, BM = Cf::BM;
   constexpr int N = M * C;
-  constexpr bool RES = MODE == AZ_RESID || MODE == AZ_GRAD;   // two transforms, scatter
+  constexpr bool RES = az_is_res(MODE);   // two transforms, scatter
   // BS (TAIL, one stage): b_{i-1} of the output rows arrives by TMA into the stage buffer once the
   // local transform has read it; the next panel's stage load is issued after the epilogue
   constexpr bool BS = az_is_tail(MODE) && NS == 1;
@@ -599,7 +624,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #else
   constexpr bool PP = (RES && Cf::XS) || BS;
 #endif
-  constexpr bool AUX = MODE == AZ_RESID || MODE == AZ_GRAD || (az_is_tail(MODE) && !BS) || MODE == AZ_INV_MASK ||
+  constexpr bool AUX = az_is_res(MODE) || (az_is_tail(MODE) && !BS) || MODE == AZ_INV_MASK ||
                       MODE == AZ_NORM;
   static_assert(C > 1, "cluster kernel");
   constexpr bool DEFER = kAzDefer<MODE> && !RES && !AUX && !BS && NS == 1;
@@ -712,9 +737,15 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   };
   uint32_t s2 = 0u;
   float sig = 0.f;
-  if constexpr (az_is_thr(MODE) || MODE == AZ_GRAD) {
+  uint32_t s2f = 0u;
+  float sigf = 0.f;
+  if constexpr (az_is_thr(MODE) || MODE == AZ_GRAD || MODE == AZ_FUSE) {
     s2 = a.st->sigma2_bits;
     sig = a.st->sigma;
+  }
+  if constexpr (MODE == AZ_FUSE) {
+    s2f = a.st->sigma2_fixed_bits;
+    sigf = a.st->sigma_fixed;
   }
   float racc = 0.f;
 
@@ -966,7 +997,7 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           ax[p][q].v = ybuf[q * (M / C) * W + p * T + t];
-          z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc, slot_k(p) + M * q, col0 + slot_w(p), s2);
+          z[p][q] = Ops::mid(a, z[p][q], ax[p][q], racc, slot_k(p) + M * q, col0 + slot_w(p), s2, sig, s2f, sigf);
         }
         const int pr = p * T + t;
         const int k = rank * (M / C) + pr / W;
@@ -1075,6 +1106,12 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
     if (it > 0) defer_finish(cid + (it - 1) * ncl, it - 1);   // the last panel (its arrive is unpaired:
     if (it > 0) cl_wait();                                     //  pair it before leaving)
   }
+  if constexpr (MODE == AZ_FUSE) {                 // support of X_{i+1} (integer-valued float counts)
+    unsigned long long cnt = (unsigned long long)racc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&a.st->support_fixed, cnt);
+  }
   if constexpr (Ops::RED) {
     float v = racc;
 #pragma unroll
@@ -1159,7 +1196,7 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
                          : az_is_tail(MODE) ? CSSAR_AZ_PROMO_TAIL : -1);
   if (e != cudaSuccess) return e;
   CUtensorMap tmy = tm;
-  if constexpr (MODE == AZ_RESID || MODE == AZ_GRAD || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b with
+  if constexpr (az_is_res(MODE) || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b with
     // consecutive rows ({col, 0, row}), box {W, 1, min(M/C, 256)}
     e = make_az_tensor_map(&tmy, MODE == AZ_RESID ? (const void*)a.Y : (const void*)a.b, n_rg, 1 << LOGN, 1, Cf::W,
                            Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256, CSSAR_AZ_PROMO_Y);
@@ -1201,7 +1238,7 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
 
 template <int LOGN, int MODE>
 static cudaError_t az_launch(int n_rg, const AzArgs& a_in, cudaStream_t s) {
-  using Cf = AzShape<LOGN, MODE == AZ_RESID || MODE == AZ_GRAD>;
+  using Cf = AzShape<LOGN, az_is_res(MODE)>;
   AzArgs a = a_in;
   if (!a.dst[0]) {                       // plain output array (single rank / in-place paths)
     a.dst[0] = a.out;
@@ -1265,6 +1302,7 @@ cudaError_t az_dispatch_mode(int mode, int n_rg, const AzArgs& a, cudaStream_t s
     case AZ_TAIL: return az_launch<LOGN, AZ_TAIL>(n_rg, a, s);
     case AZ_GRAD: return az_launch<LOGN, AZ_GRAD>(n_rg, a, s);
     case AZ_NORM: return az_launch<LOGN, AZ_NORM>(n_rg, a, s);
+    case AZ_FUSE: return az_launch<LOGN, AZ_FUSE>(n_rg, a, s);
     case AZ_FWD_SS:
     case AZ_TAIL_SS:
     case AZ_TAIL_SSD:

@@ -153,7 +153,10 @@ enum AzMode : int {
   AZ_FWD_SS = 9,      // S1: X = E(b; sigma) from the list, scattered into the stage; F_eta
   AZ_TAIL_SS = 10,    // S5: X_i from the list; b_i = X_i + mu dX -> histogram, candidates, new list
   AZ_TAIL_SSD = 11,   // S5 re-run after a select fallback: dense b_i into a.b (early exit otherwise)
+  // fixed-lambda rule (sigma known in advance, eq. 7): S5 fused with the next iteration's S1
+  AZ_FUSE = 12,       // F_eta^-1 u -> b_i = E(b_{i-1}) + mu dX (stored), X_{i+1} = E(b_i; sigma) -> F_eta
 };
+constexpr bool az_is_res(int m) { return m == AZ_RESID || m == AZ_GRAD || m == AZ_FUSE; }   // two transforms
 constexpr bool az_is_thr(int m) { return m == AZ_FWD_THR || m == AZ_FWD_SS; }
 constexpr bool az_is_tail(int m) { return m == AZ_TAIL || m == AZ_TAIL_SS || m == AZ_TAIL_SSD; }
 constexpr bool az_is_ss(int m) { return m == AZ_FWD_SS || m == AZ_TAIL_SS || m == AZ_TAIL_SSD; }

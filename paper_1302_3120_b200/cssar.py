@@ -38,6 +38,7 @@ CSSAR_FLAG_ADAPTIVE_MU = 2
 CSSAR_FLAG_SPARSE_X = 4
 CSSAR_FLAG_PEER_TRANSPOSE = 8
 CSSAR_FLAG_SPARSE_STATE = 16
+CSSAR_FLAG_FUSE_LAMBDA = 32
 STAGES = ("S1_az_head", "S2_rg_G", "S3_az_resid", "S4_rg_M", "S5_az_tail", "S6_select")
 
 
@@ -280,10 +281,11 @@ class Plan:
 
     def ita_iterate(self, Y, mask_bits, *, thr="soft", rule="k", k=0, lam=0.0, mu=1.0, iters=1, X=None,
                     log=False, profile_stages=False, stream=None, tol=0.0, sparse=False, peer=False, check=True,
-                    sparse_state=False):
+                    sparse_state=False, fuse_lambda=False):
         """Algorithm 1: X <- E(X + mu M(Theta o (Y - G X))) `iters` times, in place on X.
         mu="adaptive": the eq. 27 step rule (CSSAR_FLAG_ADAPTIVE_MU).  tol > 0: stop after the
         first update with ||X_(i+1) - X_i|| <= tol ||X_i|| (self.iters_done = updates performed).
+        fuse_lambda=True fuses S5 with the next S1 under the fixed-lambda rule (CSSAR_FLAG_FUSE_LAMBDA).
         sparse_state=True requests the sparse-state list schedule (world 1, NEXT-3; see
         include/cssar.h CSSAR_FLAG_SPARSE_STATE).
         world > 1: peer=True requests the fused peer-memory transposes (CSSAR_FLAG_PEER_TRANSPOSE),
@@ -300,7 +302,8 @@ class Plan:
                          int(k), float(lam), 1.0 if adaptive else float(mu), int(iters),
                          (CSSAR_FLAG_PROFILE_STAGES if profile_stages else 0) |
                          (CSSAR_FLAG_ADAPTIVE_MU if adaptive else 0) | (CSSAR_FLAG_SPARSE_X if sparse else 0) |
-                         (CSSAR_FLAG_PEER_TRANSPOSE if peer else 0) | (CSSAR_FLAG_SPARSE_STATE if sparse_state else 0),
+                         (CSSAR_FLAG_PEER_TRANSPOSE if peer else 0) | (CSSAR_FLAG_SPARSE_STATE if sparse_state else 0) |
+                         (CSSAR_FLAG_FUSE_LAMBDA if fuse_lambda else 0),
                          float(tol))
         logbuf = (IterLogC * max(1, iters))() if log else None
         rc = self.lib.cssar_ita_iterate(self.h, _ptr(Y), _ptr(mask_bits), ctypes.byref(prm), _ptr(X),

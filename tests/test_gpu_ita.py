@@ -388,3 +388,37 @@ def test_sparse_state_schedule_is_bitwise_the_dense_schedule(shape, iters):
     assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
     assert out[0][1] == out[1][1]
     assert out[0][2] == out[1][2] and out[1][2] >= 1      # the fallback path ran (iteration 0 at least)
+
+
+@pytest.mark.parametrize("name,iters", [("c0", 20), ("c1", 30), ("c2", 30)])
+def test_fixed_lambda_fused_schedule(name, iters):
+    """Fixed-lambda rule (eq. 7): the fused S5 + next-S1 sweep (AZ_FUSE, CSSAR_FLAG_FUSE_LAMBDA)
+    vs the unfused schedule (the same iterates up to floating-point order: <= 1e-5) and, for the
+    soft threshold (continuous, so boundary pixels cannot jump), vs the fp64 oracle (rel-L2 <=
+    1e-3, support logs within a few pixels).  lambda: 1.01 x the sigma a short k-rule run
+    reaches (away from that run's order statistic)."""
+    prob = problem(name)
+    cfg = prob.cfg
+    pl = _plan(cfg.params)
+    Yd, mb = to_dev(prob.Y), mask_bits_dev(prob.mask)
+    _, klog = pl.ita_iterate(Yd, mb, thr=cfg.thr, rule="k", k=cfg.k, mu=cfg.mu, iters=10, log=True)
+    lam = ita.lambda_from_sigma(1.01 * klog[-1]["sigma"], cfg.mu, cfg.thr)
+    Xf, lf = pl.ita_iterate(Yd, mb, thr=cfg.thr, rule="lambda", lam=lam, mu=cfg.mu, iters=iters, log=True,
+                            fuse_lambda=True)
+    Xu, lu = pl.ita_iterate(Yd, mb, thr=cfg.thr, rule="lambda", lam=lam, mu=cfg.mu, iters=iters, log=True)
+    Xf, Xu = to_host(Xf), to_host(Xu)
+    assert rel_l2(Xf, Xu) <= 1e-5
+    # the fused sweep's other FFT factorisation may flip a pixel whose |b| is within rounding of sigma
+    assert max(abs(a["support"] - b["support"]) for a, b in zip(lf, lu)) <= 2
+    if cfg.thr != "soft":
+        return
+    op = oracle_op(cfg.params)
+    olog = []
+    Xo = ita.ita(op, prob.Y.astype(np.complex128), prob.mask, thr=cfg.thr, rule="lambda", lam=lam, mu=cfg.mu,
+                 iters=iters, log=olog)
+    assert rel_l2(Xf, Xo) <= TOL_ITA
+    so = np.array([e["support"] for e in olog])
+    sf = np.array([e["support"] for e in lf])
+    assert np.max(np.abs(sf - so)) <= max(2, 1e-4 * cfg.k)
+    ro = np.array([e["resid2"] for e in olog])
+    assert np.max(np.abs(np.array([e["resid2"] for e in lf]) - ro) / ro) <= 1e-4
