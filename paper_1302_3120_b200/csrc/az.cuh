@@ -1062,10 +1062,16 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
       }
     }
-    if constexpr (MODE == AZ_TAIL || MODE == AZ_TAIL_SS) {   // flush this panel's candidates (+ list entries)
+    if constexpr (MODE == AZ_TAIL || MODE == AZ_TAIL_SS) {
+      // flush the SMEM candidates once the buffer is half full (and at the end of the kernel;
+      // a burst beyond it spills straight to the global list) and, sparse state, the panel's
+      // list entries (stored per panel)
       if (a.rule == RULE_K) {
         __syncthreads();
-        const uint32_t nc = min(tc.scount[0], (uint32_t)Cf::CAND_SMEM);
+        const uint32_t c0 = tc.scount[0];
+        const bool fc = c0 >= (uint32_t)Cf::CAND_SMEM / 2;       // uniform: read after the barrier
+        if (fc || MODE == AZ_TAIL_SS) {
+        const uint32_t nc = fc ? min(c0, (uint32_t)Cf::CAND_SMEM) : 0u;
         uint32_t nl = 0;
         if constexpr (MODE == AZ_TAIL_SS) nl = min(tc.scount[2], (uint32_t)kSlCap);
         if (t == 0) {
@@ -1084,8 +1090,9 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
         }
         __syncthreads();
         if (t == 0) {
-          tc.scount[0] = 0u;
+          if (fc) tc.scount[0] = 0u;
           tc.scount[2] = 0u;
+        }
         }
       }
     }
@@ -1130,6 +1137,13 @@ __global__ void __launch_bounds__(AzClShape<LOGN, MODE>::T, AzClShape<LOGN, MODE
   if constexpr (MODE == AZ_TAIL || MODE == AZ_TAIL_SS) {
     __syncthreads();
     if (a.rule == RULE_K) {
+      const uint32_t nc = min(tc.scount[0], (uint32_t)Cf::CAND_SMEM);   // candidates still in SMEM
+      if (t == 0) misc[32] = nc ? atomicAdd(&a.st->cand_count, nc) : 0u;
+      __syncthreads();
+      for (uint32_t i = t; i < nc; i += T) {
+        const uint32_t g = misc[32] + i;
+        if (g < a.cand_cap) a.cand[g] = tc.scand[i]; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
+      }
       for (int i = t; i < HIST_BINS; i += T) {
         const uint32_t c = tc.shist[i];
         if (c) atomicAdd(&a.hist[i], c);
