@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(T) xchg(int panels, float* sink) {
   constexpr int ELEMS = BYTES / 8;                             // float2 elements pushed per CTA
   for (int p = 0; p < panels; ++p) {
     // element e goes to owner e / (ELEMS / C), slot rank * (ELEMS / C) + e % (ELEMS / C)
-    if (VEC == 2) {
+    if (VEC == 0) {
+    } else if (VEC == 2) {
       for (int e = t; e < ELEMS; e += T) {
         const uint32_t own = (uint32_t)(e / (ELEMS / C));
         const uint32_t off = (uint32_t)((rank * (ELEMS / C) + e % (ELEMS / C)) * 8);
@@ -56,6 +57,19 @@ __global__ void __launch_bounds__(T) xchg(int panels, float* sink) {
         asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
                      ::"r"(mapa(base + off, own)), "f"((float)e), "f"((float)p), "f"((float)e + 1), "f"((float)p),
                        "r"(mapa(bb, own)) : "memory");
+      }
+    }
+    if (VEC == 0) {
+      // bulk DSMEM copies: the CTA's 32 KB source (in SMEM after the receive buffer), one
+      // cp.async.bulk of BYTES/C per owner, issued by one thread (the TMA engine moves it)
+      const uint32_t src = base + BYTES;
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int q = 0; q < C; ++q)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(mapa(base + rank * (BYTES / C), (uint32_t)q)), "r"(src + q * (BYTES / C)), "r"(BYTES / C),
+                "r"(mapa(bb, (uint32_t)q)) : "memory");
       }
     }
     asm volatile("{ .reg .pred q; WT: mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1; @!q bra WT; }"
@@ -101,12 +115,17 @@ void run(int per_sm) {
   CK(cudaEventSynchronize(b));
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double bytes = (double)ncl * C * panels * 32768.0 * (C - 1) / C;    // remote bytes
-  printf("C=%2d v%d T=%d clusters=%d: %.3f ms, remote %.0f GB/s (%.1f B/cyc/SM at 1.965 GHz over %d CTAs)\n", C, VEC,
+  printf("C=%2d %s T=%d clusters=%d: %.3f ms, remote %.0f GB/s (%.1f B/cyc/SM at 1.965 GHz over %d CTAs)\n", C,
+         VEC == 0 ? "bulk" : VEC == 2 ? "v2  " : "v4  ",
          T, ncl, ms, bytes / ms / 1e6, bytes / (ms * 1e-3) / 1.965e9 / (ncl * C / 2.0), ncl * C);
   (void)per_sm;
 }
 
 int main() {
+  run<16, 0, 256>(2);
+  run<8, 0, 256>(2);
+  run<4, 0, 256>(2);
+  run<2, 0, 256>(2);
   run<16, 2, 256>(2);
   run<16, 4, 256>(2);
   run<8, 2, 256>(2);
