@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   float2* tab = s + N * C::B;                 // exp(2 pi i h / 256) for the phase generator
   const float2* tw = tab + 256;               // inter-pass twiddles
   const int t = threadIdx.x;
+#if defined(CSSAR_PHASE_TABLE)
   copy_table_async(tab, a.tab, C::TAB, t, C::T);
+#else
+  copy_table_async(tab + 256, a.tab + 256, C::TAB - 256, t, C::T);   // the exp table serves CSSAR_PHASE_TABLE only
+#endif
   // fused-transpose destinations in SMEM: a dynamically indexed kernel-parameter array would
   // be copied to local memory (the multi-GPU variants spilled 300+ bytes per thread)
   __shared__ float2* sdst[16];
