@@ -53,7 +53,12 @@ CSSAR_DEV constexpr bool plan_ok(int logn, int E) {
   return (E == 32 && logn >= 7 && logn <= 15) || (E == 16 && logn >= 7 && logn <= 12);
 }
 
-template <int LOGN, int B, int T, bool BMINOR, int E_ = 32>
+// PIO_ (paired I/O, row engines): the first forward pass and the last reverse pass give each
+// thread two ADJACENT butterfly groups j, j + 1 (g = 2t + m) instead of g = m T + t, so the
+// caller's global loads / stores of those passes are 16-byte accesses of (j, j + 1) pairs; the
+// exchange written by the first pass XOR-swizzles with the index bits one position higher
+// (pairs of groups share a row of banks), which keeps its writes conflict-free.
+template <int LOGN, int B, int T, bool BMINOR, int E_ = 32, bool PIO_ = false>
 struct Engine {
   static constexpr int N = 1 << LOGN;
   static constexpr int E = E_;
@@ -148,16 +153,24 @@ struct Engine {
     }
   }
 
-  template <int LNS, int LR>
+  // (the first forward pass and the last reverse pass both have radix plan_lr(LOGN, E, 0))
+  static constexpr bool PIO = PIO_ && !BMINOR && P >= 2;
+  static_assert(!PIO || (E / (1 << plan_lr(LOGN, E, 0))) % 2 == 0,
+                "paired I/O needs an even number of groups per thread in the first / last passes");
+
+  template <int LNS, int LR, int SH = 0>
   static CSSAR_DEV int swz(int i) {
     constexpr int NS = 1 << LNS;
-    if constexpr (NS >= G || LNS + LR >= LOGN) {
+    if constexpr (NS >= G || LNS + LR + SH >= LOGN) {
       return i;
     } else {
       constexpr int mask = G / NS - 1;
-      return i ^ (((i >> (LNS + LR)) & mask) << LNS);
+      return i ^ (((i >> (LNS + LR + SH)) & mask) << LNS);
     }
   }
+  // butterfly group of thread t's m-th group: m T + t, or (paired) 2 ((m / 2) T + t) + m % 2
+  template <bool PM>
+  static CSSAR_DEV int gmap(int m, int t) { return PM ? 2 * ((m >> 1) * T + t) + (m & 1) : m * T + t; }
   static CSSAR_DEV int addr(int b, int i) { return BMINOR ? i * B + b : b * N + i; }
 
   template <int R>
@@ -168,7 +181,7 @@ struct Engine {
 
   // butterflies of one pass on registers v (E elements: group m at v[m*R .. m*R+R));
   // tw = this pass's SMEM twiddle table (required for passes with NS > 1)
-  template <int LR, int LNS, int DIR>
+  template <int LR, int LNS, int DIR, bool PM = false>
   static CSSAR_DEV void butterflies(float2 (&v)[E], int t, const float2* tw) {
     constexpr int R = 1 << LR, NS = 1 << LNS, L = NS * R;
 #if defined(CSSAR_EXP_NOFFT_AZ)
@@ -177,7 +190,7 @@ struct Engine {
 #pragma unroll
     for (int m = 0; m < E / R; ++m) {
       int b, j;
-      bj<R>(m * T + t, b, j);
+      bj<R>(gmap<PM>(m, t), b, j);
       float2 x[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = v[m * R + r];
@@ -207,41 +220,62 @@ struct Engine {
   }
 
   // write pass output (writer LR, LNS) to SMEM, swizzled for this exchange
-  template <int LR, int LNS>
+  template <int LR, int LNS, bool PM = false, int SH = 0>
   static CSSAR_DEV void write(float2* s, const float2 (&v)[E], int t) {
     constexpr int R = 1 << LR, NS = 1 << LNS;
 #pragma unroll
     for (int m = 0; m < E / R; ++m) {
       int b, j;
-      bj<R>(m * T + t, b, j);
+      bj<R>(gmap<PM>(m, t), b, j);
       const int base = (j >> LNS) * (NS * R) + (j & (NS - 1));
 #pragma unroll
-      for (int r = 0; r < R; ++r) s[addr(b, swz<LNS, LR>(base + r * NS))] = v[m * R + r];
+      for (int r = 0; r < R; ++r) s[addr(b, swz<LNS, LR, SH>(base + r * NS))] = v[m * R + r];
     }
   }
 
-  // read the input of a pass with radix 2^LR from SMEM written by exchange (WLR, WLNS)
-  template <int LR, int WLR, int WLNS>
+  // read the input of a pass with radix 2^LR from SMEM written by exchange (WLR, WLNS, WSH);
+  // PM (paired groups j, j + 1 of one row) with an unswizzled exchange: one 16-byte load per pair
+  template <int LR, int WLR, int WLNS, int WSH = 0, bool PM = false>
   static CSSAR_DEV void read(const float2* s, float2 (&v)[E], int t) {
     constexpr int R = 1 << LR;
+    constexpr bool VEC = PM && ((1 << WLNS) >= G || WLNS + WLR + WSH >= LOGN);   // identity swizzle
+    if constexpr (VEC) {
 #pragma unroll
-    for (int m = 0; m < E / R; ++m) {
-      int b, j;
-      bj<R>(m * T + t, b, j);
+      for (int m = 0; m < E / R; m += 2) {
+        int b, j;
+        bj<R>(gmap<PM>(m, t), b, j);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[m * R + r] = s[addr(b, swz<WLNS, WLR>(j + r * (N / R)))];
+        for (int r = 0; r < R; ++r) {
+          const float4 q = *reinterpret_cast<const float4*>(&s[addr(b, j + r * (N / R))]);
+          v[m * R + r] = make_float2(q.x, q.y);
+          v[(m + 1) * R + r] = make_float2(q.z, q.w);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < E / R; ++m) {
+        int b, j;
+        bj<R>(gmap<PM>(m, t), b, j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[m * R + r] = s[addr(b, swz<WLNS, WLR, WSH>(j + r * (N / R)))];
+      }
     }
   }
 
-  template <int LR, class F>
+  template <int LR, class F, bool PM = false>
   static CSSAR_DEV void for_groups(float2 (&v)[E], int t, F&& f) {
     constexpr int R = 1 << LR;
 #pragma unroll
     for (int m = 0; m < E / R; ++m) {
       int b, j;
-      bj<R>(m * T + t, b, j);
+      bj<R>(gmap<PM>(m, t), b, j);
       f(b, j, &v[m * R]);
     }
+  }
+  // the groups of the first forward / last reverse pass (paired when PIO)
+  template <int LR, class F>
+  static CSSAR_DEV void for_io(float2 (&v)[E], int t, F&& f) {
+    for_groups<LR, F, PIO>(v, t, static_cast<F&&>(f));
   }
 
   // Passes p = P0 .. P-1 of a transform whose first pass input is already in registers.
@@ -249,14 +283,18 @@ struct Engine {
   template <int DIR, bool REV, int p>
   static CSSAR_DEV void passes_from(float2* s, float2 (&v)[E], int t, const float2* tw) {
     constexpr int LR = lr<REV>(p), LNS = lns<REV>(p);
+    // paired groups: the first forward pass (input from the caller) and the last reverse pass
+    constexpr bool PM = PIO && ((p == 0 && !REV) || (p == P - 1 && REV));
+    constexpr bool PMN = PIO && (p + 1 == P - 1 && REV);          // the next pass
+    constexpr int SH = (PIO && p == 0 && !REV) ? 1 : 0;            // swizzle shift of this exchange
     if constexpr (p == 0 && !REV) cp_async_wait_all();   // async table staging (no-op if none)
-    butterflies<LR, LNS, DIR>(v, t, tw + tw_off<REV>(p));
+    butterflies<LR, LNS, DIR, PM>(v, t, tw + tw_off<REV>(p));
     if constexpr (p + 1 < P) {
       __syncthreads();                 // everyone finished reading the previous exchange
 #if defined(CSSAR_EXP_NOXCH_AZ)
       if constexpr (!BMINOR) {         // experiment: azimuth passes without the SMEM exchange
 #endif
-      write<LR, LNS>(s, v, t);
+      write<LR, LNS, PM, SH>(s, v, t);
 #if defined(CSSAR_EXP_NOXCH_AZ)
       }
 #endif
@@ -264,7 +302,7 @@ struct Engine {
 #if defined(CSSAR_EXP_NOXCH_AZ)
       if constexpr (!BMINOR)
 #endif
-      read<lr<REV>(p + 1), LR, LNS>(s, v, t);
+      read<lr<REV>(p + 1), LR, LNS, SH, PMN>(s, v, t);
       passes_from<DIR, REV, p + 1>(s, v, t, tw);
     }
   }
@@ -275,7 +313,7 @@ struct Engine {
   static CSSAR_DEV void run(float2* s, Load&& ld, Store&& st, const float2* tw) {
     const int t = threadIdx.x;
     float2 v[E];
-    for_groups<lr<false>(0)>(v, t, ld);
+    for_io<lr<false>(0)>(v, t, ld);
     passes_from<DIR, false, 0>(s, v, t, tw);
     for_groups<lr<false>(P - 1)>(v, t, st);
   }
@@ -285,18 +323,18 @@ struct Engine {
   static CSSAR_DEV void conv(float2* s, Load&& ld, Mid&& mid, Store&& st, const float2* tw) {
     const int t = threadIdx.x;
     float2 v[E];
-    for_groups<lr<false>(0)>(v, t, ld);
+    for_io<lr<false>(0)>(v, t, ld);
     passes_from<DIR, false, 0>(s, v, t, tw);
     for_groups<lr<false>(P - 1)>(v, t, mid);
     passes_from<-DIR, true, 0>(s, v, t, tw);
-    for_groups<lr<true>(P - 1)>(v, t, st);
+    for_io<lr<true>(P - 1)>(v, t, st);
   }
 
   // run() without the Store: the natural-order output groups stay in v (for cluster kernels)
   template <int DIR, class Load>
   static CSSAR_DEV void run_keep(float2* s, float2 (&v)[E], Load&& ld, const float2* tw) {
     const int t = threadIdx.x;
-    for_groups<lr<false>(0)>(v, t, ld);
+    for_io<lr<false>(0)>(v, t, ld);
     passes_from<DIR, false, 0>(s, v, t, tw);
   }
 
@@ -324,7 +362,7 @@ struct Engine {
     const int t = threadIdx.x;
     float2 v[E];
     constexpr int LR0 = lr<false>(0), R0 = 1 << LR0;
-    for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+    for_io<LR0>(v, t, [&](int b, int j, float2* x) {
 #pragma unroll
       for (int r = 0; r < R0; ++r) x[r] = s[addr(b, j + r * (N / R0))];
     });

@@ -17,7 +17,9 @@ struct RgCfg {
 #define CSSAR_RG_MINB 2
 #endif
   static constexpr int MINB = LOGN >= 14 ? 1 : CSSAR_RG_MINB;   // resident CTAs per SM (register cap)
-  using En = Engine<LOGN, B, T, false, E>;
+  // paired I/O (16-byte row loads / stores) where the first radix leaves two groups per thread
+  static constexpr bool PIO = (E / (1 << plan_lr(LOGN, E, 0))) % 2 == 0;
+  using En = Engine<LOGN, B, T, false, E, PIO>;
   static constexpr int TAB = 256 + En::TW_TOTAL;                // phase table + twiddle tables
   static constexpr size_t SMEM = sizeof(float2) * (N * B + TAB);
 };
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
       }
     }
     __syncthreads();
-    En::template for_groups<LR0>(vv, tt, [&](int b, int j, float2* x) {
+    En::template for_io<LR0>(vv, tt, [&](int b, int j, float2* x) {
 #pragma unroll
       for (int r = 0; r < R0; ++r) x[r] = sm[b * N + rsw(j + r * (N / R0))];
     });
@@ -211,19 +213,34 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   };
   pdl_wait();                                 // the previous sweep's output is complete
   for (; row0 < nrows; row0 += (int)gridDim.x * C::B) {
-  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {      // raw row loads
+  if constexpr (En::PIO && !BLK) {            // raw row loads, 16 bytes (groups j, j + 1) each
 #pragma unroll
-    for (int r = 0; r < R0; ++r) x[r] = data[at(row0 + b, j + r * (N / R0))];
-  });
+    for (int m = 0; m < En::E / R0; m += 2) {
+      int b, j;
+      En::template bj<R0>(En::template gmap<true>(m, t), b, j);
+      const float2* src = data + (size_t)(row0 + b) * N + j;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const float4 q = *reinterpret_cast<const float4*>(src + r * (N / R0));
+        v[m * R0 + r] = make_float2(q.x, q.y);
+        v[(m + 1) * R0 + r] = make_float2(q.z, q.w);
+      }
+    }
+  } else {
+    En::template for_io<LR0>(v, t, [&](int b, int j, float2* x) {    // raw row loads
+#pragma unroll
+      for (int r = 0; r < R0; ++r) x[r] = data[at(row0 + b, j + r * (N / R0))];
+    });
+  }
   cp_async_wait_all();
   __syncthreads();                            // tables visible; the previous rows' SMEM reads done
   if constexpr (!RDA) {
-    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // prologue phase
+    En::template for_io<LR0>(v, t, [&](int b, int j, float2* x) {    // prologue phase
       const Quad q = a.coef[grow(row0 + b)].q[GBODY ? 2 : 0];
       phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
     });
   } else if constexpr (GBODY) {
-    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage the row
+    En::template for_io<LR0>(v, t, [&](int b, int j, float2* x) {    // P_eta*, stage the row
       phase_apply<R0, N / R0, true>(tab, a.coef[grow(row0 + b)].q[2], j - N / 2, x);
 #pragma unroll
       for (int r = 0; r < R0; ++r) s[b * N + rsw(j + r * (N / R0))] = x[r];
@@ -258,14 +275,14 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
   En::template passes_from<+1, true, 0>(s, v, t, tw);                    // range IFFT
   if constexpr (RDA && !GBODY) {                                          // C on the whole row
     __syncthreads();                    // every thread finished reading the last exchange
-    En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+    En::template for_io<LR0>(v, t, [&](int b, int j, float2* x) {
 #pragma unroll
       for (int r = 0; r < R0; ++r) s[b * N + rsw(j + r * (N / R0))] = x[r];
     });
     __syncthreads();
     rcmc_apply(std::false_type{}, s, v, t);
   }
-  En::template for_groups<LR0>(v, t, [&](int b, int j, float2* x) {
+  En::template for_io<LR0>(v, t, [&](int b, int j, float2* x) {
     if constexpr (!RDA) {
       const Quad q = a.coef[grow(row0 + b)].q[GBODY ? 0 : 2];
       phase_apply<R0, N / R0, GBODY>(tab, q, j - N / 2, x);
@@ -285,9 +302,24 @@ __global__ void __launch_bounds__(RgCfg<LOGN>::T, RgCfg<LOGN>::MINB) rg_sweep_ke
         return;
       }
     }
+    if constexpr (!(En::PIO && !BLK)) {
 #pragma unroll
-    for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
+      for (int r = 0; r < R0; ++r) data[at(row0 + b, j + r * (N / R0))] = x[r];   // 1/n_rg folded into AzArgs::oscale
+    }
   });
+  if constexpr (En::PIO && !BLK) {            // row stores, 16 bytes (groups j, j + 1) each
+#pragma unroll
+    for (int m = 0; m < En::E / R0; m += 2) {
+      int b, j;
+      En::template bj<R0>(En::template gmap<true>(m, t), b, j);
+      float2* dst = data + (size_t)(row0 + b) * N + j;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const float2 lo = v[m * R0 + r], hi = v[(m + 1) * R0 + r];
+        *reinterpret_cast<float4*>(dst + r * (N / R0)) = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+    }
+  }
   }
   pdl_launch_dependents();                   // (at the end: dependents may not run ahead)
   if constexpr (BLK) {
