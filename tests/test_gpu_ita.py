@@ -192,6 +192,23 @@ def test_ita_zero_echo_and_nonfinite():
     with pytest.raises(CssarError) as e:
         pl.ita_iterate(Y, None, thr="soft", rule="k", k=5, iters=2, log=True)
     assert e.value.code == -6
+    # without a log: reported by cssar_ita_status (the binding checks it unless check=False)
+    with pytest.raises(CssarError) as e:
+        pl.ita_iterate(Y, None, thr="soft", rule="k", k=5, iters=2)
+    assert e.value.code == -6
+    pl.ita_iterate(Y, None, thr="soft", rule="k", k=5, iters=2, check=False)
+    with pytest.raises(CssarError) as e:
+        pl.status()
+    assert e.value.code == -6
+    # a clean solve afterwards reports OK again; and on a cluster-shape grid (n_az = 2048)
+    Y[3, 4] = 0.0
+    pl.ita_iterate(Y, None, thr="soft", rule="k", k=5, iters=2)
+    pl2 = _plan(SarParams(n_az=2048, n_rg=256))
+    Y2 = torch.zeros((2048, 256), dtype=torch.complex64, device="cuda")
+    Y2[100, 7] = float("inf")
+    with pytest.raises(CssarError) as e:
+        pl2.ita_iterate(Y2, None, thr="soft", rule="k", k=50, iters=2)
+    assert e.value.code == -6
 
 
 def test_ita_fallback_only_when_window_misses():
@@ -422,3 +439,22 @@ def test_fixed_lambda_fused_schedule(name, iters):
     assert np.max(np.abs(sf - so)) <= max(2, 1e-4 * cfg.k)
     ro = np.array([e["resid2"] for e in olog])
     assert np.max(np.abs(np.array([e["resid2"] for e in lf]) - ro) / ro) <= 1e-4
+
+
+@pytest.mark.parametrize("k", [100, 700000, 2000000])
+def test_select_exact_when_the_candidate_list_overflows(k):
+    """A flat |b| (1.5 M equal values in one histogram bin of a 2048^2 grid, more than the
+    n/8 + 64k candidate capacity) makes the fallback's candidate list overflow; the select then
+    counts its two 10-bit radix levels over b itself and stays exact (advisor finding r1)."""
+    from paper_1302_3120_b200 import Plan
+    from inputs.configs import SarParams
+    shape = (2048, 2048)
+    b = rand_c(shape, 31)
+    flat = b.reshape(-1)
+    flat[1000:1501000] = np.complex64(0.6 + 0.8j)          # |b| = 1 exactly, 1.5 M times
+    flat[2000000:2000010] = 0
+    pl = Plan(SarParams(n_az=shape[0], n_rg=shape[1]))
+    s2, above = pl.debug_select(to_dev(b), k)
+    m = np.sort(mag2_f32(b).reshape(-1))[::-1]
+    assert s2 == int(m[k].view(np.uint32))
+    assert above == int(np.count_nonzero(m > m[k]))
