@@ -169,12 +169,14 @@ def measure_c4(args, peak, peak_kind):
     dom = max((s for s in STAGES if s != "S6_select"), key=lambda s: stages[s])
     dom_ach = BYTES_PER_SAMPLE[dom] * n / (stages[dom] * 1e-3) / 1e9
     iter_ach = ITER_BYTES_PER_SAMPLE * n * it_s / 1e9
+    tf = os.path.join(ROOT, "profiles", "traffic_c4.json")
+    traffic = json.load(open(tf)).get(dom) if os.path.exists(tf) else None
     out = {"workload": f"c4: {p.n_az}x{p.n_rg} complex64, Fr {p.Fr / 1e6:.0f} MHz, {cfg.scene} scene, {cfg.mask} "
                        f"mask {cfg.rate}, SNR {cfg.snr_db} dB, soft threshold, k = {cfg.k}",
            "value": n * it_s, "unit": "samples*it/s", "ms_per_step": ms / steps, "it_per_s": it_s, "steps": steps,
            "stages_ms": stages,
            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak, "unit": "GB/s",
-                        "frac": dom_ach / peak, "peak_kind": peak_kind,
+                        "frac": dom_ach / peak, "traffic": traffic, "peak_kind": peak_kind,
                         "algorithmic_bytes_per_launch": BYTES_PER_SAMPLE[dom] * n, "avg_launch_ms": stages[dom]},
            "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak, "unit": "GB/s",
                                   "frac": iter_ach / peak, "bytes_per_sample": ITER_BYTES_PER_SAMPLE},

@@ -1193,19 +1193,26 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
     }
   }
   CUtensorMap tm;
-  // the head sweep's panel loads: 64-byte L2 promotion (measured 0.391 -> 0.381 ms at c3; the
-  // other sweeps are fastest with the default 256 B)
+  // L2 promotion of the TMA panel loads (measured at c3, profiles/experiments_r02.md):
+  //  * head sweep: 64 B (0.391 -> 0.381 ms);
+  //  * residual sweep, U and Y: 64 B -- same time as 256 B, but DRAM reads 1.346 -> 1.086 GB per
+  //    launch (the algorithmic 1.082 GB): with 256 B the 64-byte panel rows pulled in lines of
+  //    neighbouring panels that were evicted before their cluster reached them;
+  //  * tail sweep (U and b): the default 256 B (64 B on b: 0.566 -> 0.60 ms).
+#if !defined(CSSAR_AZ_PROMO_HEAD)
+#define CSSAR_AZ_PROMO_HEAD 1
+#endif
 #if !defined(CSSAR_AZ_PROMO_RESID)
-#define CSSAR_AZ_PROMO_RESID -1
+#define CSSAR_AZ_PROMO_RESID 1
 #endif
 #if !defined(CSSAR_AZ_PROMO_TAIL)
 #define CSSAR_AZ_PROMO_TAIL -1
 #endif
 #if !defined(CSSAR_AZ_PROMO_Y)
-#define CSSAR_AZ_PROMO_Y -1
+#define CSSAR_AZ_PROMO_Y 1
 #endif
   e = make_az_tensor_map(&tm, a.in, n_rg, 1 << LOGN, Cf::C, Cf::W, Cf::BM,
-                         MODE == AZ_FWD_THR ? (int)CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         MODE == AZ_FWD_THR ? CSSAR_AZ_PROMO_HEAD
                          : MODE == AZ_RESID ? CSSAR_AZ_PROMO_RESID
                          : az_is_tail(MODE) ? CSSAR_AZ_PROMO_TAIL : -1);
   if (e != cudaSuccess) return e;
@@ -1213,7 +1220,8 @@ static cudaError_t az_cluster_launch(int n_rg, const AzArgs& a, cudaStream_t s) 
   if constexpr (az_is_res(MODE) || (MODE == AZ_TAIL && Cf::NS == 1)) {   // Y (RESID) / b with
     // consecutive rows ({col, 0, row}), box {W, 1, min(M/C, 256)}
     e = make_az_tensor_map(&tmy, MODE == AZ_RESID ? (const void*)a.Y : (const void*)a.b, n_rg, 1 << LOGN, 1, Cf::W,
-                           Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256, CSSAR_AZ_PROMO_Y);
+                           Cf::M / Cf::C < 256 ? Cf::M / Cf::C : 256,
+                           MODE == AZ_RESID ? CSSAR_AZ_PROMO_Y : CSSAR_AZ_PROMO_TAIL);
     if (e != cudaSuccess) return e;
   }
   const int npan = n_rg / Cf::W;
