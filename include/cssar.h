@@ -300,6 +300,13 @@ int cssar_debug_ipc_open(const void* rec, void** base_out, void** ptr_out);
 int cssar_debug_ipc_close(void* base);
 int cssar_debug_peer_store(void* dst, uint32_t pattern, int64_t n_words, void* stream);
 int cssar_group_debug_barrier(cssar_group group, int32_t rounds, void* stream);
+/* A world-1 plan over a ONE-rank NCCL communicator (nccl_unique_id: 128 bytes from
+ * cssar_nccl_unique_id) that runs the slab path of cssar_plan_create(world > 1) -- the
+ * all-to-all transposes (ncclSend / ncclRecv to itself in a group), the grouped all-reduces
+ * of the select, the IPC all-gather of cssar_bind_workspace -- with whole arrays as slabs, so
+ * the real NCCL plumbing can be checked on one GPU against the world-1 path (bitwise equal
+ * results).  Same contract as a world > 1 plan otherwise (debug hooks: CSSAR_ERR_BAD_PLAN). */
+int cssar_debug_plan_create_nccl(cssar_plan* out, const cssar_sar_params* p, const void* nccl_unique_id);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,9 @@ struct cssar_plan_s {
   int world = 1, rank = 0;
   long long nrow = 0, ncol = 0;     // row slab: nrow = n_az/world lines; column slab: ncol = n_rg/world gates
   int transport = 0;                // kTransportNone / kTransportNccl / kTransportGroup
+  // the slab path (row / column slabs, transposes, rank-reduced select) runs: world > 1, or a
+  // one-rank NCCL plan (cssar_debug_plan_create_nccl, a test of the NCCL plumbing on one GPU)
+  bool multi = false;
   ncclComm_t comm = nullptr;
   uint32_t* d_lvl = nullptr;        // 1024 level counts of the split fine select
   // workspace views (world > 1): column slabs [n_az][ncol], blocked row slab [world][nrow][ncol]
@@ -825,10 +828,10 @@ int validate_ita(cssar_plan pl, const cssar_ita_params* prm) {
   if (prm->rule == CSSAR_RULE_FIXED_LAMBDA && (!(prm->lambda >= 0.0) || !std::isfinite(prm->lambda)))
     return CSSAR_ERR_BAD_MU;
   if (prm->iters < 0 || prm->iters > kLogCap) return CSSAR_ERR_INVALID_PARAMS;
-  if ((prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && pl->world != 1) return CSSAR_ERR_INVALID_PARAMS;
-  if (!(prm->tol >= 0.0) || !std::isfinite(prm->tol) || (prm->tol > 0.0 && pl->world != 1))
+  if ((prm->flags & CSSAR_FLAG_ADAPTIVE_MU) && pl->multi) return CSSAR_ERR_INVALID_PARAMS;
+  if (!(prm->tol >= 0.0) || !std::isfinite(prm->tol) || (prm->tol > 0.0 && pl->multi))
     return CSSAR_ERR_INVALID_PARAMS;
-  if ((prm->flags & CSSAR_FLAG_SPARSE_X) && pl->world == 1) return CSSAR_ERR_INVALID_PARAMS;
+  if ((prm->flags & CSSAR_FLAG_SPARSE_X) && !pl->multi) return CSSAR_ERR_INVALID_PARAMS;
   return CSSAR_OK;
 }
 
@@ -1056,9 +1059,9 @@ int map_peers_nccl(cssar_plan pl) {
   return CSSAR_OK;
 }
 
-int validate_world(const cssar_sar_params& p, int world, int rank) {
+int validate_world(const cssar_sar_params& p, int world, int rank, bool multi) {
   if (world < 1 || world > 16 || rank < 0 || rank >= world) return CSSAR_ERR_BAD_PLAN;
-  if (world == 1) return CSSAR_OK;
+  if (!multi) return CSSAR_OK;
   if (p.n_az % world || p.n_rg % world) return CSSAR_ERR_UNSUPPORTED_SIZE;
   const long long nrow = p.n_az / world, ncol = p.n_rg / world;
   const int rpc = rg_rows_per_cta(ilog2_exact(p.n_rg));
@@ -1073,7 +1076,8 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
   *out = nullptr;
   int v = validate_params(*p);
   if (v != CSSAR_OK) return v;
-  v = validate_world(*p, world, rank);
+  const bool multi = world > 1 || transport == kTransportNccl;
+  v = validate_world(*p, world, rank, multi);
   if (v != CSSAR_OK) return v;
   cssar_plan pl = new cssar_plan_s();
   pl->p = *p;
@@ -1085,6 +1089,7 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
   pl->nrow = p->n_az / world;
   pl->ncol = p->n_rg / world;
   pl->transport = transport;
+  pl->multi = multi;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -1127,7 +1132,7 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
     return CSSAR_ERR_CUDA;
   }
   pl->h_nonfinite[0] = pl->h_nonfinite[1] = 0u;
-  if (world > 1 && pl->log_naz - ilog2_exact(world) >= 7 &&
+  if (multi && pl->log_naz - ilog2_exact(world) >= 7 &&
       (cudaMalloc(&pl->d_az_tab_m, sizeof(float2) * (az_table_count(pl->log_naz - ilog2_exact(world), false) + 2)) !=
            cudaSuccess ||
        az_table_fill(pl->log_naz - ilog2_exact(world), false, pl->d_az_tab_m, pl->cap_stream) != cudaSuccess ||
@@ -1135,7 +1140,7 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
-  if (world > 1 && (cudaMalloc(&pl->d_bar, 16) != cudaSuccess || cudaMemset(pl->d_bar, 0, 16) != cudaSuccess)) {
+  if (multi && (cudaMalloc(&pl->d_bar, 16) != cudaSuccess || cudaMemset(pl->d_bar, 0, 16) != cudaSuccess)) {
     cssar_plan_destroy(pl);
     return CSSAR_ERR_CUDA;
   }
@@ -1164,13 +1169,13 @@ size_t sx_bytes(size_t nl) { return align256(kSxHeader + sizeof(SxEntry) * (nl /
 // array per panel + its counter)
 size_t ss_bytes(cssar_plan pl) {
   const int W = az_panel_width(pl->log_naz);
-  if (pl->world != 1 || W <= 0) return 0;
+  if (pl->multi || W <= 0) return 0;
   const size_t npan = (size_t)(pl->p.n_rg / W);
   return 2 * (align256(sizeof(SsEntry) * (size_t)pl->n) + align256(sizeof(uint32_t) * npan));
 }
 
 size_t workspace_bytes(cssar_plan pl) {
-  if (pl->world == 1)
+  if (!pl->multi)
     return align256(3 * sizeof(float2) * (size_t)pl->n + sizeof(uint32_t) * cand_capacity(pl->n)) + ss_bytes(pl) + 256;
   const size_t nl = (size_t)pl->p.n_az * (size_t)pl->ncol;
   return 4 * align256(sizeof(float2) * nl) + align256(nl / 8) + align256(sizeof(uint32_t) * cand_capacity((long long)nl)) +
@@ -1178,7 +1183,7 @@ size_t workspace_bytes(cssar_plan pl) {
 }
 
 void bind_views(cssar_plan pl, char* ws) {
-  if (pl->world == 1) {
+  if (!pl->multi) {
     pl->U = (float2*)ws;
     pl->D = (float2*)(ws + sizeof(float2) * (size_t)pl->n);
     pl->Xk = (float2*)(ws + 2 * sizeof(float2) * (size_t)pl->n);
@@ -1235,6 +1240,11 @@ int cssar_plan_create(cssar_plan* out, const cssar_sar_params* p, int world, int
   return plan_create_impl(out, p, world, rank, world > 1 ? kTransportNccl : kTransportNone, nccl_unique_id);
 }
 
+int cssar_debug_plan_create_nccl(cssar_plan* out, const cssar_sar_params* p, const void* nccl_unique_id) {
+  if (!out || !p || !nccl_unique_id) return CSSAR_ERR_BAD_PLAN;
+  return plan_create_impl(out, p, 1, 0, kTransportNccl, nccl_unique_id);
+}
+
 int cssar_nccl_unique_id(void* id_out) {
   if (!id_out) return CSSAR_ERR_BAD_PLAN;
   NcclApi& n = nccl();
@@ -1249,8 +1259,14 @@ int cssar_plan_destroy(cssar_plan pl) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   close_peers(pl);
   cudaFree(pl->d_bar);
-  if (pl->comm && nccl().ok) nccl().commDestroy(pl->comm);
+  // the cached graph first: NCCL work captured in it holds the communicator (ncclCommDestroy
+  // waits for the graph's release of it -- measured: a hang when destroyed in the other order)
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+  pl->gexec = nullptr;
+  if (pl->comm && nccl().ok) {
+    cudaDeviceSynchronize();
+    nccl().commDestroy(pl->comm);
+  }
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   for (int i = 0; i < 7; ++i)
     if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
@@ -1367,7 +1383,7 @@ int cssar_group_ita_iterate(cssar_group g, const void* const* Y, const uint32_t*
 int cssar_forward(cssar_plan pl, const void* X, const uint32_t* mask_bits, void* Y_out, void* stream) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(X) || !aligned16(Y_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
-  if (pl->world > 1) {
+  if (pl->multi) {
     Ranks R{&pl, 1};
     return op_multi(R, true, &X, &mask_bits, &Y_out, (cudaStream_t)stream);
   }
@@ -1377,7 +1393,7 @@ int cssar_forward(cssar_plan pl, const void* X, const uint32_t* mask_bits, void*
 int cssar_adjoint(cssar_plan pl, const void* R, const uint32_t* mask_bits, void* X_out, void* stream) {
   if (!pl) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(R) || !aligned16(X_out) || (mask_bits && !aligned16(mask_bits))) return CSSAR_ERR_ALIGNMENT;
-  if (pl->world > 1) {
+  if (pl->multi) {
     Ranks Rk{&pl, 1};
     return op_multi(Rk, false, &R, &mask_bits, &X_out, (cudaStream_t)stream);
   }
@@ -1418,7 +1434,7 @@ int cssar_ita_iterate(cssar_plan pl, const void* Y, const uint32_t* mask_bits, c
   if (!pl->U) return CSSAR_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   pl->iters_done = prm->iters;
-  if (pl->world > 1) {                          // this rank's row slabs; NCCL transposes
+  if (pl->multi) {                              // this rank's row slabs; NCCL transposes
     Ranks R{&pl, 1};
     const int rc = ita_multi(R, &Y, &mask_bits, *prm, &X_inout, log_host, s, &pl->gexec, &pl->gkey, &pl->ghave);
     if (rc == CSSAR_OK && pl->comm && nccl().asyncError) {     // failure detection
@@ -1617,7 +1633,7 @@ int cssar_pack_mask(const uint8_t* mask_u8, uint32_t* mask_bits, int64_t rows, i
 }
 
 int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
-  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->multi) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(U)) return CSSAR_ERR_ALIGNMENT;
   RgArgs r{(float2*)U, pl->d_coef, 0, pl->d_rg_tab};
   r.rcmc = pl->d_rcmc;
@@ -1627,7 +1643,7 @@ int cssar_debug_range_sweep(cssar_plan pl, void* U, int gbody, void* stream) {
 }
 
 int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* stream) {
-  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->multi) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(in) || !aligned16(out)) return CSSAR_ERR_ALIGNMENT;
   AzArgs a{};
   a.tw = pl->d_az_tab;
@@ -1643,7 +1659,7 @@ int cssar_debug_az_fft(cssar_plan pl, const void* in, void* out, int dir, void* 
 
 int cssar_debug_select(cssar_plan pl, const void* b, int64_t k, uint32_t* sigma2_bits_out, int64_t* above_out,
                        void* stream) {
-  if (!pl || pl->world != 1) return CSSAR_ERR_BAD_PLAN;
+  if (!pl || pl->multi) return CSSAR_ERR_BAD_PLAN;
   if (!aligned16(b)) return CSSAR_ERR_ALIGNMENT;
   if (k < 1 || k >= pl->n) return CSSAR_ERR_BAD_K;
   if (!pl->U) return CSSAR_ERR_WORKSPACE;

@@ -31,7 +31,7 @@ SYMBOLS = [
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
     "cssar_ita_iters_done", "cssar_plan_set_pulse", "cssar_group_operator", "cssar_ita_status",
     "cssar_debug_ipc_export", "cssar_debug_ipc_open", "cssar_debug_ipc_close", "cssar_debug_peer_store",
-    "cssar_group_debug_barrier",
+    "cssar_group_debug_barrier", "cssar_debug_plan_create_nccl",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
@@ -108,6 +108,7 @@ def load_library(path=None):
     lib.cssar_debug_ipc_close.argtypes = [V]
     lib.cssar_debug_peer_store.argtypes = [V, ctypes.c_uint32, I64, V]
     lib.cssar_group_debug_barrier.argtypes = [P, ctypes.c_int32, V]
+    lib.cssar_debug_plan_create_nccl.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SarParamsC), V]
     lib.cssar_plan_set_pulse.argtypes = [P, V, I64]
     lib.cssar_group_operator.argtypes = [P, I, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(V), V]
     lib.cssar_group_bind_workspace.argtypes = [P, I, V, ctypes.c_size_t]
@@ -215,7 +216,9 @@ class Plan:
         """world > 1: this process is `rank` of a slab-partitioned plan; its
         arrays are row slabs of n_az/world azimuth lines; unique_id = the 128-byte NCCL id
         (nccl_unique_id() on one rank, shared by the caller, e.g. dist.broadcast_object_list).
-        op: "csa" (north star) or "rda" (NEXT-2, the paper's CSRDA pair, eq. 14-18)."""
+        op: "csa" (north star) or "rda" (NEXT-2, the paper's CSRDA pair, eq. 14-18).
+        world == 1 with a unique_id: a one-rank NCCL plan that runs the slab path (a test of the
+        NCCL plumbing on one GPU, cssar_debug_plan_create_nccl)."""
         self.lib = load_library()
         self.params = params
         self.op = op
@@ -224,12 +227,16 @@ class Plan:
         h = ctypes.c_void_p()
         pc = _params_c(params, op)
         uid = None
-        if self.world > 1:
+        if self.world > 1 or unique_id is not None:
             if unique_id is None or len(unique_id) != 128:
                 raise ValueError("world > 1 needs the 128-byte NCCL unique id")
             uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-        _check(self.lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(pc), self.world, self.rank, uid,
-                                          _stream(stream)), "cssar_plan_create")
+        if self.world == 1 and uid is not None:     # one-rank NCCL plan on the slab path (test hook)
+            _check(self.lib.cssar_debug_plan_create_nccl(ctypes.byref(h), ctypes.byref(pc), uid),
+                   "cssar_debug_plan_create_nccl")
+        else:
+            _check(self.lib.cssar_plan_create(ctypes.byref(h), ctypes.byref(pc), self.world, self.rank, uid,
+                                              _stream(stream)), "cssar_plan_create")
         self.h = h
         self.ws = None
         if workspace:
