@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-sparse-state", action="store_true", help="skip the sparse-state (NEXT-3) object")
     ap.add_argument("--peer-transpose", action="store_true",
                     help="N > 1: fused peer-memory transposes and the sparse-X' sweep (not yet validated on >1 GPU)")
+    ap.add_argument("--slab", action="store_true",
+                    help="diagnostic: at N = 1 run the multi-rank slab path over a one-rank NCCL communicator "
+                         "(transposes to itself) instead of the single-GPU schedule")
     return ap.parse_args()
 
 
@@ -260,11 +263,27 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "samples*it/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "samples*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The ONE JSON line on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # keep stdout for the JSON line alone: anything else written to fd 1 (NCCL's version
+    # banner, library chatter) goes to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -288,17 +307,19 @@ def main():
     Y, mb, mask, sc = make_problem_gpu(cfg, plan)
     X = torch.zeros_like(Y)
     kw = dict(thr=cfg.thr, rule=cfg.rule, k=cfg.k, lam=cfg.lam, mu=cfg.mu)
-    if world > 1 and args.peer_transpose:
+    slab = world > 1 or args.slab
+    if slab and args.peer_transpose:
         # fused peer-memory transposes + sparse-X' first sweep (CSSAR_FLAG_PEER_TRANSPOSE |
         # CSSAR_FLAG_SPARSE_X); default: NCCL all-to-all transposes (validated path)
         kw["peer"] = True
         kw["sparse"] = True
-    if world > 1:
+    if slab:
         # strong scaling: ONE scene slab-partitioned by azimuth lines; NCCL
         # all-to-all transposes inside libcssar, communicator from a broadcast unique id
         from paper_1302_3120_b200 import nccl_unique_id, slab_rows
         uid = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         lo, hi = slab_rows(p.n_az, world, rank)
         Y = Y[lo:hi].contiguous()
         mb = mb[lo:hi].contiguous()
@@ -334,7 +355,7 @@ def main():
     # per-step breakdown (CUDA events on the launch stream inside the library)
     stages = None
     roof = None
-    if not args.no_profile and world == 1:
+    if not args.no_profile and not slab:
         kp = max(3, min(args.steps, 30))
         plan.ita_iterate(Y, mb, X=X, iters=kp, profile_stages=True, **kw)
         st_ms, it_meas = plan.stage_times()
@@ -360,15 +381,16 @@ def main():
         "config": {"workload": f"{args.config}{'' if args.op == 'csa' else ' [RDA pair]'}: {p.n_az}x{p.n_rg} complex64, {cfg.scene} scene, {cfg.mask} mask "
                                f"{cfg.rate}, SNR {cfg.snr_db} dB, {cfg.thr} threshold, k = {cfg.k}, mu = {cfg.mu}",
                    "n_az": p.n_az, "n_rg": p.n_rg, "k": cfg.k, "l2": "inputs larger than L2 (512 MiB arrays)",
-                   "parallelism": "single" if world == 1 else
-                   f"slab{world} (azimuth-line row slabs; transposes fused into the sweeps as peer-memory "
-                   f"stores, or NCCL all-to-all; sparse-X' S1; reduced select)"},
+                   "parallelism": "single" if not slab else
+                   f"slab{world} (azimuth-line row slabs; " + ("transposes fused into the sweeps as peer-memory "
+                   "stores, sparse-X' S1" if args.peer_transpose else "NCCL all-to-all transposes") +
+                   "; rank-reduced select" + ("; one-rank NCCL diagnostic)" if world == 1 else ")")},
         "roofline": roof,
         "iteration_roofline": {"bound": "hbm", "achieved": iter_ach, "peak": peak * world, "unit": "GB/s",
                                "frac": iter_ach / (peak * world), "bytes_per_sample": ITER_BYTES_PER_SAMPLE,
                                "note": "aggregate over ranks; excludes NVLink transpose bytes" if world > 1 else None},
         "stages_ms": stages,
-        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if world == 1 else
+        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if not slab else
                                        ((14 if world <= 8 else 12) if cfg.rule == "k" else 6)) + 2,
         "select_fallbacks": plan.debug_fallbacks(),
         "clocks": clocks,
@@ -398,7 +420,7 @@ def main():
         line["e2e"] = {"value": n * iters / dt, "unit": "samples*it/s", "h2d_bytes_per_step": h2d / iters,
                        "d2h_bytes_per_step": d2h / iters, "solve_iters": iters,
                        "note": "one full reconstruction (config iteration count) per call; copies once per solve"}
-    if world == 1 and not args.no_sparse_state and cfg.rule == "k":
+    if not slab and not args.no_sparse_state and cfg.rule == "k":
         # NEXT-3 sparse-state schedule (CSSAR_FLAG_SPARSE_STATE) on the same workload: 72.125
         # algorithmic HBM B/sample instead of 96.125 (the dense b traffic of S1 and S5 removed)
         plan.ita_iterate(Y, mb, X=X, iters=max(3, args.warmup), sparse_state=True, **kw)
@@ -409,18 +431,18 @@ def main():
                                 "unit": "samples*it/s", "bytes_per_sample": 72.125,
                                 "iteration_achieved_GBps": 72.125 * n * it_ss / 1e9, "stages_ms": st_ss,
                                 "note": "opt-in schedule; bitwise the dense schedule's results"}
-    if world == 1 and not args.no_c4 and args.config == "c3":
+    if not slab and not args.no_c4 and args.config == "c3":
         del Y, X
         torch.cuda.empty_cache()
         line["c4"] = measure_c4(args, peak, peak_kind)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not slab and not args.no_cpu_baseline:
         # the oracle on the full c3 grid (one ITA iteration; ~10-30 s of host work)
         line["cpu_baseline"] = cpu_baseline(args.config, p.n_az, p.n_rg, 1)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     return 0
 
 
