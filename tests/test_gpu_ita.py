@@ -458,3 +458,46 @@ def test_select_exact_when_the_candidate_list_overflows(k):
     m = np.sort(mag2_f32(b).reshape(-1))[::-1]
     assert s2 == int(m[k].view(np.uint32))
     assert above == int(np.count_nonzero(m > m[k]))
+
+
+@pytest.mark.parametrize("case", ["mask0", "iters0", "k1", "kmax", "delta"])
+def test_ita_degenerate_cases(case):
+    """Degenerate inputs of Algorithm 1 on a 256 x 512 grid:
+    mask0  -- Theta = 0 everywhere: the residual vanishes, X stays 0 whatever Y holds;
+    iters0 -- no iteration: X is returned untouched (bitwise);
+    k1     -- the k-rule keeps one pixel (sigma = the 2nd largest |b|), vs the oracle;
+    kmax   -- k = n - 1 (sigma = the smallest |b|), vs the oracle;
+    delta  -- a single-pixel echo, vs the oracle."""
+    import torch
+    from inputs.configs import SarParams
+    p = SarParams(n_az=256, n_rg=512)
+    n = p.n_az * p.n_rg
+    Y = rand_c((p.n_az, p.n_rg), 11)
+    mask = np.ones((p.n_az, p.n_rg), dtype=bool)
+    k, iters = 50, 4
+    if case == "mask0":
+        mask[:] = False
+    elif case == "k1":
+        k = 1
+    elif case == "kmax":
+        k = n - 1
+    elif case == "delta":
+        Y = np.zeros_like(Y)
+        Y[37, 101] = 3.0 - 2.0j
+    pl = _plan(p)
+    X0 = to_dev(rand_c((p.n_az, p.n_rg), 12)) if case == "iters0" else None
+    Xg = pl.ita_iterate(to_dev(Y), mask_bits_dev(mask), thr="soft", rule="k", k=k, mu=1.0,
+                        iters=0 if case == "iters0" else iters,
+                        X=None if X0 is None else X0.clone())
+    Xg = to_host(Xg)
+    if case == "iters0":
+        assert np.array_equal(Xg.view(np.uint32), to_host(X0).view(np.uint32))
+        return
+    if case == "mask0":
+        assert not np.any(Xg)
+        return
+    Xo = ita.ita(csa.CSAOperator(p), Y.astype(np.complex128), mask, thr="soft", rule="k", k=k, mu=1.0, iters=iters)
+    assert rel_l2(Xg, Xo) <= 1e-4, rel_l2(Xg, Xo)
+    assert np.count_nonzero(Xg) <= k
+    if case != "kmax":
+        assert set(np.flatnonzero(Xg).tolist()) == set(np.flatnonzero(Xo).tolist())
