@@ -178,6 +178,16 @@ CSSAR_DEV void red_commit(double* part, uint32_t* ticket, double* target, float 
   }
 }
 
+// candidate straight to the global list (the tail's SMEM buffer is full)
+static __device__ __noinline__ void cand_spill(SelState* st, uint32_t* cand, uint32_t cap, uint32_t* hist, uint32_t u) {
+  const uint32_t g = atomicAdd(&st->cand_count, 1u);
+  if (g < cap) cand[g] = u; else { st->cand_overflow = 1u; hist[HIST_BINS] = 1u; }
+}
+static __device__ __noinline__ void flag_nonfinite(SelState* st, uint32_t* hist) {
+  st->nonfinite = 1u;
+  hist[HIST_BINS + 1] = 1u;
+}
+
 template <int MODE>
 struct AzOps {
   static constexpr int DIR = (MODE <= AZ_FWD_THR || MODE == AZ_FWD_SS) ? -1 : +1;   // first transform direction
@@ -295,7 +305,8 @@ struct AzOps {
     }
   }
 
-  // histogram / candidates / support of one new b (TAIL)
+  // histogram / candidates / support of one new b (TAIL); the rare paths (SMEM candidate
+  // buffer full, non-finite value) are out of line to keep the unrolled epilogue small
   CSSAR_DEV static void tail_stats(const AzArgs& a, float2 bn, TailCtx& tc) {
     const uint32_t u = mag2_bits(bn);
     const int bin = (int)(u >> HIST_SHIFT);
@@ -303,17 +314,13 @@ struct AzOps {
       if (bin >= tc.floor_bin) atomicAdd(&tc.shist[bin], 1u);
       if (bin >= tc.cand_lo && bin <= tc.cand_hi) {
         const uint32_t pos = atomicAdd(&tc.scount[0], 1u);
-        if (pos < 1024u) {
-          tc.scand[pos] = u;
-        } else {
-          const uint32_t g = atomicAdd(&a.st->cand_count, 1u);
-          if (g < a.cand_cap) a.cand[g] = u; else { a.st->cand_overflow = 1u; a.hist[HIST_BINS] = 1u; }
-        }
+        if (pos < 1024u) tc.scand[pos] = u;
+        else cand_spill(a.st, a.cand, a.cand_cap, a.hist, u);
       }
-      if (bin >= (0x7F800000u >> HIST_SHIFT)) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
+      if (bin >= (0x7F800000u >> HIST_SHIFT)) flag_nonfinite(a.st, a.hist);
     } else {
       if (u > tc.s2fixed) atomicAdd(&tc.scount[1], 1u);
-      if (u >= 0x7F800000u) { a.st->nonfinite = 1u; a.hist[HIST_BINS + 1] = 1u; }
+      if (u >= 0x7F800000u) flag_nonfinite(a.st, a.hist);
     }
   }
 

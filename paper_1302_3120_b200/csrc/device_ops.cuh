@@ -31,17 +31,18 @@ CSSAR_DEV float rsqrt_ftz(float x) {
   return r;
 }
 
-// E(b; sigma): strict survival on the fp32 |b|^2 pattern (DESIGN.md "Selection rule"),
-// soft (eq. 9), half (q = 1/2), hard (q = 0) or q = 2/3 shrink of the magnitude, phase kept.
-CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
-  const uint32_t u = mag2_bits(b);
-  const float a2 = __uint_as_float(u);
+// shrink factor of the q = 2/3 and q = 1/2 thresholds (closed forms with transcendental
+// functions).  Out of line by default: inlined at every element of the unrolled sweep
+// epilogues they made the azimuth kernels' code several times larger than the soft / hard
+// path that runs (instruction-cache stalls); CSSAR_THR_INLINE=1 restores inlining.
+#if defined(CSSAR_THR_INLINE) && CSSAR_THR_INLINE
+#define CSSAR_THR_HEAVY CSSAR_DEV
+#else
+#define CSSAR_THR_HEAVY static __device__ __noinline__
+#endif
+CSSAR_THR_HEAVY float thr_factor_heavy(float a2, float sigma, int thr) {
   float f;
-  if (thr == THR_SOFT) {
-    f = sigma == 0.f ? 1.0f : fmaf(-sigma, rsqrt_ftz(a2), 1.0f);   // 1 - sigma/|b|
-  } else if (thr == THR_HARD) {
-    f = 1.0f;
-  } else if (thr == THR_TWOTHIRDS) {
+  if (thr == THR_TWOTHIRDS) {
     // closed-form L2/3 minimiser in k-rule form (oracle/ita.py twothirds): q = 27 t^2 /
     // (16 lm^(3/2)) = (3 sqrt(3)/4)(t/sigma)^2, phi = c sigma^(1/3) sqrt(cosh(acosh(q)/3))
     const float t = a2 * rsqrt_ftz(a2);
@@ -55,6 +56,22 @@ CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
     const float phi = acosf(0.70710678118654752f * ratio * sqrtf(ratio));
     f = (2.0f / 3.0f) * (1.0f + cosf(2.09439510239319549f - (2.0f / 3.0f) * phi));
     f = sigma == 0.f ? 1.0f : f;
+  }
+  return f;
+}
+
+// E(b; sigma): strict survival on the fp32 |b|^2 pattern (DESIGN.md "Selection rule"),
+// soft (eq. 9), half (q = 1/2), hard (q = 0) or q = 2/3 shrink of the magnitude, phase kept.
+CSSAR_DEV float2 threshold(float2 b, uint32_t s2bits, float sigma, int thr) {
+  const uint32_t u = mag2_bits(b);
+  const float a2 = __uint_as_float(u);
+  float f;
+  if (thr == THR_SOFT) {
+    f = sigma == 0.f ? 1.0f : fmaf(-sigma, rsqrt_ftz(a2), 1.0f);   // 1 - sigma/|b|
+  } else if (thr == THR_HARD) {
+    f = 1.0f;
+  } else {
+    f = thr_factor_heavy(a2, sigma, thr);
   }
   // strict survival on the |b|^2 pattern; a removed entry is +0 (not b * 0, whose sign would
   // follow b: the sparse-state schedule's zero-filled X must equal the dense one bitwise).
