@@ -98,6 +98,7 @@ struct AzArgs {
   float2* dst[16];
   int dlog_nrow;
   int drank;
+  int dsingle;              // set by launch_az: one destination (dst[0] + row n_rg + col)
   float2* D;                // AZ_GRAD: dense gradient dX (for the elementwise step)
   float lambda;             // fixed-lambda rule with the adaptive step (sigma_i = f(lambda mu_i))
   // deterministic squared-norm reductions (RESID / GRAD / NORM): per-CTA partials in slot
