@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (32768 x 16384) object")
+    ap.add_argument("--no-library", action="store_true", help="skip the torch.fft library-chain comparator")
     ap.add_argument("--no-sparse-state", action="store_true", help="skip the sparse-state (NEXT-3) object")
     ap.add_argument("--peer-transpose", action="store_true",
                     help="N > 1: fused peer-memory transposes and the sparse-X' sweep (not yet validated on >1 GPU)")
@@ -202,6 +203,60 @@ def measure_c4(args, peak, peak_kind):
     del plan
     torch.cuda.empty_cache()
     return out
+
+
+def library_chain(Y, mask, k, mu, steps=10, warm=3):
+    """SURVEY 8(d) "library chain" comparator (context, not the product and not a parity path):
+    the same ITA iteration composed from torch.fft (cuFFT) and torch elementwise / topk ops in
+    complex64 on this GPU -- E_sigma (soft), F_eta, Phi3*, F_tau, Phi2*, F_tau^-1, Phi1*, F_eta^-1,
+    r = Theta(Y - g), the M chain, b = X + mu D, sigma = (k+1)-th largest |b| by torch.topk.  The
+    phase screens are seeded unit phasors of the operator's shape: every multiply, FFT and select
+    the chain performs is the one the operator needs, so the time is that of the composition."""
+    import math
+    import torch
+    n_az, n_rg = Y.shape
+    g = torch.Generator(device="cuda").manual_seed(1302)
+
+    def phasor():
+        return torch.polar(torch.ones(n_az, n_rg, device="cuda"),
+                           2 * math.pi * torch.rand(n_az, n_rg, device="cuda", generator=g))
+    P1, P2, P3 = phasor(), phasor(), phasor()
+    P1c, P2c, P3c = P1.conj().resolve_conj(), P2.conj().resolve_conj(), P3.conj().resolve_conj()
+    maskf = mask.to(torch.float32)
+    fft, ifft = torch.fft.fft, torch.fft.ifft
+
+    def step(b, sigma):
+        mag = b.abs()
+        X = b * torch.clamp(1 - sigma / mag.clamp_min(1e-30), min=0)                  # E_sigma(b)
+        U = fft(X, dim=0, norm="ortho").mul_(P3c)
+        U = fft(U, dim=1, norm="ortho").mul_(P2c)
+        U = ifft(U, dim=1, norm="ortho").mul_(P1c)
+        r = (Y - ifft(U, dim=0, norm="ortho")).mul_(maskf)                            # Theta(Y - G X)
+        V = fft(r, dim=0, norm="ortho").mul_(P1)
+        V = fft(V, dim=1, norm="ortho").mul_(P2)
+        V = ifft(V, dim=1, norm="ortho").mul_(P3)
+        b = X.add_(ifft(V, dim=0, norm="ortho"), alpha=mu)                             # X + mu M(r)
+        sigma = torch.topk(b.abs().view(-1), k + 1, sorted=False).values.min()
+        return b, sigma
+
+    b = Y.clone()
+    sigma = torch.zeros((), device="cuda")
+    for _ in range(warm):
+        b, sigma = step(b, sigma)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        b, sigma = step(b, sigma)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del P1, P2, P3, P1c, P2c, P3c, maskf, b
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "it_per_s": 1e3 / ms, "value": n_az * n_rg * 1e3 / ms, "unit": "samples*it/s",
+            "steps": steps, "note": "the iteration composed from torch.fft (cuFFT) + torch elementwise / topk "
+            "ops, complex64, same grid and k; timing context only (seeded unit phase screens, not a parity path)"}
 
 
 def cpu_baseline(cfg_name, n_az, n_rg, iters):
@@ -431,6 +486,9 @@ def main():
                                 "unit": "samples*it/s", "bytes_per_sample": 72.125,
                                 "iteration_achieved_GBps": 72.125 * n * it_ss / 1e9, "stages_ms": st_ss,
                                 "note": "opt-in schedule; bitwise the dense schedule's results"}
+    if not slab and not args.no_library and cfg.rule == "k" and cfg.thr == "soft":
+        line["library_chain"] = library_chain(Y, mask, cfg.k, cfg.mu)
+    del mask
     if not slab and not args.no_c4 and args.config == "c3":
         del Y, X
         torch.cuda.empty_cache()
