@@ -286,6 +286,15 @@ int cssar_stage_times(cssar_plan plan, double* ms_out, int32_t* iters_out);
 /* Number of full-histogram fallbacks taken by the last cssar_ita_iterate (synchronous). */
 int cssar_debug_fallbacks(cssar_plan plan, int32_t* out, void* stream);
 
+/* Multi-GPU select: *info_out = 1 when the cached iteration graph of a world > 1
+ * plan (or of an emulation group's ranks) runs the select's full-histogram fallback round -- a
+ * pass over b, one 2048-word all-reduce and the pick -- as a conditional graph node that only
+ * executes when the coarse step missed its window (3 collectives per iteration instead of 4),
+ * 0 when the round is captured unconditionally (world 1, no graph yet, or the conditional capture
+ * failed and the library fell back).  Host-only, no synchronisation. */
+int cssar_debug_graph_info(cssar_plan plan, int32_t* info_out);
+int cssar_group_debug_graph_info(cssar_group group, int32_t* info_out);
+
 /* Multi-GPU plumbing hooks (tests).  cssar_debug_ipc_export writes an 80-byte
  * record {cudaIpcMemHandle_t of the allocation holding dev_ptr, byte offset of dev_ptr in it,
  * pad} -- the same record cssar_bind_workspace all-gathers; cssar_debug_ipc_open maps a peer

@@ -68,6 +68,9 @@ struct cssar_plan_s {
   uint32_t cand_cap = 0;
   // graph cache for the iteration body
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cond_stream = nullptr;   // captures the body of the conditional fallback round (world > 1)
+  bool cond_ok = true;                  // conditional graph nodes usable (cleared if a capture with one fails)
+  bool cond_used = false;               // the cached iteration graph gates the fallback round
   cudaGraphExec_t gexec = nullptr;
   GraphKey gkey{};
   bool ghave = false;
@@ -594,6 +597,11 @@ RgArgs rg_row_args(cssar_plan pl) {
   return r;
 }
 
+// the select's fallback round runs when the coarse step set need_full (conditional graph node)
+__global__ void set_fallback_cond_kernel(cudaGraphConditionalHandle h, const SelState* st) {
+  cudaGraphSetConditional(h, st->need_full ? 1u : 0u);
+}
+
 // one ITA iteration (S1..S6) of every rank in R
 int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s, bool sparse = false) {
   cssar_plan p0 = R.pl[0];
@@ -641,12 +649,12 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
                                  s));
     return CSSAR_OK;
   };
-  auto local_sel = [&](int part) -> int {
+  auto local_sel = [&](int part, cudaStream_t ss) -> int {
     for (int i = 0; i < R.np; ++i) {
       cssar_plan pl = R.pl[i];
       CUDA_TRY(launch_select_part(part, pl->sm_count, pl->bcol, pl->p.n_az * pl->ncol, prm.k, prm.thr,
                                   (float)prm.mu, pl->d_st, pl->d_hist, pl->d_hist_full, pl->cand, pl->cand_cap,
-                                  pl->d_lvl, pl->d_log, kLogCap, s));
+                                  pl->d_lvl, pl->d_log, kLogCap, ss));
     }
     return CSSAR_OK;
   };
@@ -726,17 +734,56 @@ int iteration_multi(const Ranks& R, const cssar_ita_params& prm, cudaStream_t s,
   if (prm.rule == CSSAR_RULE_KSPARSE) {       // S6: exact (k+1)-th largest over all ranks
     // ||r||^2 and the |b|^2 histogram (+ flags) in one NCCL group: one collective launch
     STEP(xchg_allreduce2(R, B, 2, 1, H, 0, HIST_WORDS, s));
-    STEP(local_sel(SEL_COARSE));
-    STEP(local_sel(SEL_FB_HIST));
-    gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist_full; });
-    STEP(xchg_allreduce(R, B, 0, HIST_BINS, s));
-    STEP(local_sel(SEL_FB_PICK));
-    STEP(local_sel(SEL_FINE0_HIST));
+    STEP(local_sel(SEL_COARSE, s));
+    // full-histogram fallback round (the coarse bin missed the speculative window): a pass over
+    // b, an all-reduce of 2048 words and the pick.  Every rank takes the same decision from the
+    // same reduced counts, so inside a captured iteration it is a conditional graph node whose
+    // body runs only when need_full is set -- 3 collectives per iteration instead of 4
+    auto fb_round = [&](cudaStream_t ss) -> int {
+      STEP(local_sel(SEL_FB_HIST, ss));
+      gather_ptrs(R, B, [](cssar_plan q) { return q->d_hist_full; });
+      STEP(xchg_allreduce(R, B, 0, HIST_BINS, ss));
+      STEP(local_sel(SEL_FB_PICK, ss));
+      return CSSAR_OK;
+    };
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive && p0->cond_ok && p0->cond_stream && !getenv("CSSAR_NO_COND")) {
+      cudaGraph_t g = nullptr;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      CUDA_TRY(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+      cudaGraphConditionalHandle h;
+      CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0u, 0u));
+      set_fallback_cond_kernel<<<1, 1, 0, s>>>(h, p0->d_st);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeIf;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      CUDA_TRY(cudaGraphAddNode(&node, g, deps, nd, &cp));
+      CUDA_TRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      CUDA_TRY(cudaStreamBeginCaptureToGraph(p0->cond_stream, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal));
+      const int rb = fb_round(p0->cond_stream);
+      cudaGraph_t gb = nullptr;
+      const cudaError_t eb = cudaStreamEndCapture(p0->cond_stream, &gb);
+      STEP(rb);
+      CUDA_TRY(eb);
+      p0->cond_used = true;
+    } else {
+      STEP(fb_round(s));
+    }
+    STEP(local_sel(SEL_FINE0_HIST, s));
     gather_ptrs(R, B, [](cssar_plan q) { return q->d_lvl; });
     STEP(xchg_allreduce(R, B, 0, 1024, s));
-    STEP(local_sel(SEL_FINE0_FIND));
+    STEP(local_sel(SEL_FINE0_FIND, s));
     STEP(xchg_allreduce(R, B, 0, 1024, s));
-    STEP(local_sel(SEL_FINE1_FIND));
+    STEP(local_sel(SEL_FINE1_FIND, s));
   } else {
     void* S[16];
     gather_ptrs(R, S, [](cssar_plan q) {
@@ -924,15 +971,26 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
     if (!*ghave || !(*gkey == key)) {
       if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
       *ghave = false;
-      cudaGraph_t g = nullptr;
-      CUDA_TRY(cudaStreamBeginCapture(p0->cap_stream, cudaStreamCaptureModeThreadLocal));
-      rc = iteration_multi(R, prm, p0->cap_stream, sparse);
-      cudaError_t ec = cudaStreamEndCapture(p0->cap_stream, &g);
-      if (rc != CSSAR_OK) { if (g) cudaGraphDestroy(g); return rc; }
-      CUDA_TRY(ec);
-      cudaError_t ei = cudaGraphInstantiate(gexec, g, 0);
-      cudaGraphDestroy(g);
-      CUDA_TRY(ei);
+      // with the conditional fallback round first; if the capture or instantiation of that
+      // graph fails (e.g. collective work the conditional body cannot hold), once more without it
+      for (int attempt = 0;; ++attempt) {
+        cudaGraph_t g = nullptr;
+        p0->cond_used = false;
+        CUDA_TRY(cudaStreamBeginCapture(p0->cap_stream, cudaStreamCaptureModeThreadLocal));
+        rc = iteration_multi(R, prm, p0->cap_stream, sparse);
+        cudaError_t ec = cudaStreamEndCapture(p0->cap_stream, &g);
+        cudaError_t ei = cudaErrorUnknown;
+        if (rc == CSSAR_OK && ec == cudaSuccess) ei = cudaGraphInstantiate(gexec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (rc == CSSAR_OK && ec == cudaSuccess && ei == cudaSuccess) break;
+        if (!p0->cond_used || attempt > 0) {
+          if (rc != CSSAR_OK) return rc;
+          CUDA_TRY(ec);
+          CUDA_TRY(ei);
+        }
+        (void)cudaGetLastError();
+        p0->cond_ok = false;                   // retry with the unconditional fallback round
+      }
       *gkey = key;
       *ghave = true;
     }
@@ -1111,6 +1169,7 @@ int plan_create_impl(cssar_plan* out, const cssar_sar_params* p, int world, int 
       cudaMemset(pl->d_red, 0, sizeof(double) * (3 * kRedSlots + 8)) != cudaSuccess ||
       cudaMalloc(&pl->d_log, sizeof(IterLogDev) * kLogCap) != cudaSuccess ||
       cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&pl->cond_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&pl->d_rg_tab, sizeof(float2) * rg_table_count(pl->log_nrg)) != cudaSuccess ||
       cudaMalloc(&pl->d_az_tab, sizeof(float2) * (az_table_count(pl->log_naz, false) + 2)) != cudaSuccess ||
       cudaMalloc(&pl->d_az_tab_r, sizeof(float2) * (az_table_count(pl->log_naz, true) + 2)) != cudaSuccess ||
@@ -1268,6 +1327,7 @@ int cssar_plan_destroy(cssar_plan pl) {
     nccl().commDestroy(pl->comm);
   }
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
+  if (pl->cond_stream) cudaStreamDestroy(pl->cond_stream);
   for (int i = 0; i < 7; ++i)
     if (pl->ev[i]) cudaEventDestroy(pl->ev[i]);
   if (pl->ev_solve) cudaEventDestroy(pl->ev_solve);
@@ -1736,6 +1796,18 @@ int cssar_group_debug_barrier(cssar_group g, int32_t rounds, void* stream) {
   CUDA_TRY(cudaMemcpyAsync(&epoch0, g->pl[0]->d_bar + 1, sizeof(epoch0), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   if (e || epoch0 != (uint32_t)rounds) return CSSAR_ERR_NCCL;
+  return CSSAR_OK;
+}
+
+int cssar_debug_graph_info(cssar_plan pl, int32_t* out) {
+  if (!pl || !out) return CSSAR_ERR_BAD_PLAN;
+  *out = pl->cond_used ? 1 : 0;
+  return CSSAR_OK;
+}
+
+int cssar_group_debug_graph_info(cssar_group g, int32_t* out) {
+  if (!g || !out || g->pl.empty()) return CSSAR_ERR_BAD_PLAN;
+  *out = g->pl[0]->cond_used ? 1 : 0;
   return CSSAR_OK;
 }
 

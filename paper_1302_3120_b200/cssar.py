@@ -31,7 +31,8 @@ SYMBOLS = [
     "cssar_group_destroy", "cssar_group_workspace_size", "cssar_group_bind_workspace", "cssar_group_ita_iterate",
     "cssar_ita_iters_done", "cssar_plan_set_pulse", "cssar_group_operator", "cssar_ita_status",
     "cssar_debug_ipc_export", "cssar_debug_ipc_open", "cssar_debug_ipc_close", "cssar_debug_peer_store",
-    "cssar_group_debug_barrier", "cssar_debug_plan_create_nccl",
+    "cssar_group_debug_barrier", "cssar_debug_plan_create_nccl", "cssar_debug_graph_info",
+    "cssar_group_debug_graph_info",
 ]
 CSSAR_FLAG_PROFILE_STAGES = 1
 CSSAR_FLAG_ADAPTIVE_MU = 2
@@ -96,6 +97,8 @@ def load_library(path=None):
     lib.cssar_debug_az_fft.argtypes = [P, V, V, I, V]
     lib.cssar_debug_select.argtypes = [P, V, I64, U32P, ctypes.POINTER(ctypes.c_int64), V]
     lib.cssar_debug_fallbacks.argtypes = [P, ctypes.POINTER(ctypes.c_int32), V]
+    lib.cssar_debug_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.cssar_group_debug_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.cssar_stage_times.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]
     lib.cssar_nccl_unique_id.argtypes = [V]
     lib.cssar_group_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SarParamsC), I, V]
@@ -383,6 +386,13 @@ class Plan:
         _check(self.lib.cssar_debug_fallbacks(self.h, ctypes.byref(v), _stream(stream)), "fallbacks")
         return v.value
 
+    def debug_graph_info(self):
+        """1 when the cached multi-GPU iteration graph gates the select's fallback round with a
+        conditional node (cssar_debug_graph_info)."""
+        v = ctypes.c_int32()
+        _check(self.lib.cssar_debug_graph_info(self.h, ctypes.byref(v)), "cssar_debug_graph_info")
+        return v.value
+
 
 def _itaprm(thr, rule, k, lam, mu, iters, profile_stages=False):
     return ItaParamsC(THR_CODES[thr],
@@ -424,6 +434,12 @@ class Group:
             self.close()
         except Exception:
             pass
+
+    def debug_graph_info(self):
+        """1 when the cached iteration graph gates the fallback round with a conditional node."""
+        v = ctypes.c_int32()
+        _check(self.lib.cssar_group_debug_graph_info(self.h, ctypes.byref(v)), "cssar_group_debug_graph_info")
+        return v.value
 
     def debug_barrier(self, rounds, stream=None):
         """`rounds` flag-barrier rounds over all ranks in one cooperative launch."""

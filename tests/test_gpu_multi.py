@@ -90,6 +90,36 @@ def test_group_transports_bitwise(transport, monkeypatch):
     _same_logs(lg, ls)
 
 
+@pytest.mark.parametrize("cond", [True, False])
+def test_group_conditional_fallback_round(cond, monkeypatch):
+    """The select's full-histogram fallback round (pass over b, 2048-word all-reduce, pick) is a
+    conditional graph node in the captured multi-GPU iteration (3 collectives per iteration
+    instead of 4): its body must run exactly when the coarse step misses -- the first iteration
+    from X = 0 always does here -- so X stays bitwise the single-GPU result, with the node and
+    with the unconditional round (CSSAR_NO_COND)."""
+    import torch
+    from paper_1302_3120_b200 import Group, Plan
+    if not cond:
+        monkeypatch.setenv("CSSAR_NO_COND", "1")
+    prob = problem("c2", 1024, 1024)
+    cfg = prob.cfg
+    iters = 6
+    pl = Plan(cfg.params)
+    X1, l1 = pl.ita_iterate(to_dev(prob.Y), mask_bits_dev(prob.mask), thr=cfg.thr, rule=cfg.rule, k=cfg.k,
+                            mu=cfg.mu, iters=iters, log=True)
+    assert pl.debug_fallbacks() >= 1                 # the fallback branch is taken at least once
+    world = 4
+    g = Group(cfg.params, world)
+    Ys = [to_dev(y) for y in _slabs(prob.Y, world)]
+    Ms = [m.contiguous() for m in _slabs(mask_bits_dev(prob.mask), world)]
+    Xs = [torch.zeros_like(y) for y in Ys]
+    lg = g.ita_iterate(Ys, Ms, Xs, thr=cfg.thr, rule=cfg.rule, k=cfg.k, mu=cfg.mu, iters=iters, log=True)
+    assert g.debug_graph_info() == (1 if cond else 0)
+    Xg = np.concatenate([to_host(x) for x in Xs], axis=0)
+    assert np.array_equal(Xg.view(np.uint32), to_host(X1).view(np.uint32)), rel_l2(Xg, to_host(X1))
+    _same_logs(lg, l1)
+
+
 def test_group_fixed_lambda_and_no_mask():
     prob = problem("c2", 512, 512)
     Xs, ls = _single_run(prob, 5, rule="lambda", lam=0.05, masked=False)

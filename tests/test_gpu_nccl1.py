@@ -55,6 +55,9 @@ def test_nccl_one_rank_ita_is_bitwise_world1(name, grid, iters, peer):
     Xn, ln = _run(pn, prob, iters, peer=peer)
     assert np.array_equal(Xn.view(np.uint32), X1.view(np.uint32)), rel_l2(Xn, X1)
     _same_logs(ln, l1)
+    # the select's fallback round is a conditional graph node holding the NCCL all-reduce
+    assert pn.debug_graph_info() == 1
+    assert p1.debug_fallbacks() >= 1
 
 
 def test_nccl_one_rank_sparse_x():
