@@ -13,9 +13,11 @@ flush is needed between steps.
 
 Prints ONE JSON line (rank 0).  value = complex samples * iterations / s of the scene.
 N > 1 (torchrun): the SAME c3 scene slab-partitioned over the ranks by azimuth lines
-(transposes fused into the sweeps as peer-memory stores (NCCL all-to-all if the
-peers cannot be mapped), the sparse-X' first sweep, reduced exact select) -> "scaling":
-"strong"; the time is the max over ranks.
+(NCCL all-to-all transposes between the sweeps by default; --peer-transpose
+fuses them into the sweeps as CUDA-IPC peer-memory stores and adds the sparse-X' first sweep;
+reduced exact select, its fallback round a conditional graph node) -> "scaling": "strong";
+the time is the max over ranks.  The line also carries a "library_chain" object: the same
+iteration composed from torch.fft (cuFFT) + torch ops on this GPU (timing context).
 """
 import argparse
 import json
