@@ -333,11 +333,12 @@ def test_ita_tolerance_stop_matches_oracle(name, op):
 
 
 @pytest.mark.parametrize("n_az,n_rg,op", [(4096, 256, "csa"), (16384, 128, "csa"), (16384, 128, "rda"),
-                                          (8192, 512, "rda")])
+                                          (8192, 512, "rda"), (32768, 128, "csa")])
 def test_ita_tall_grids_every_cluster_shape(n_az, n_rg, op):
-    """Azimuth lengths whose sweeps use 4- and 16-CTA clusters (n_az 4096, 16384) and the
-    c3 shape's (8192) through the residual and tail kernels (stage / receive ping-pong),
-    4 iterations of the c2 recipe vs the oracle."""
+    """Azimuth lengths whose sweeps use 4- and 16-CTA clusters (n_az 4096, 16384, and c4's
+    32768 with its 64 KB stages at one CTA per SM) and the c3 shape's (8192) through the
+    residual and tail kernels (stage / receive ping-pong), 4 iterations of the c2 recipe vs the
+    oracle."""
     from oracle import rda
     from paper_1302_3120_b200 import Plan
     prob = problem("c2", n_az, n_rg)
