@@ -26,7 +26,8 @@ __device__ __forceinline__ uint32_t crank() {
 constexpr int BYTES = 32768;
 constexpr int V4 = BYTES / 16;          // float4 per CTA per panel
 
-// MODE 0: DSMEM, 1: L2 scratch, 2: half DSMEM / half L2.  HBM: stream 32 KB in and out per panel.
+// MODE 0: DSMEM, 1: L2 scratch, 2: half DSMEM / half L2, 3: no exchange (the HBM stream alone).
+// HBM: stream 32 KB in and out per panel.
 template <int C, int MODE, bool HBM, int T>
 __global__ void __launch_bounds__(T) xchg(int panels, float4* scratch, const float4* hin, float4* hout,
                                          size_t hbm_v4, float* sink) {
@@ -36,8 +37,8 @@ __global__ void __launch_bounds__(T) xchg(int panels, float4* scratch, const flo
   const int t = threadIdx.x;
   const uint32_t rank = crank();
   const int cid = blockIdx.x / C, ncl = gridDim.x / C;
-  constexpr int DS = MODE == 0 ? V4 : MODE == 1 ? 0 : V4 / 2;   // float4 through DSMEM
-  constexpr int L2N = V4 - DS;                                 // float4 through L2
+  constexpr int DS = MODE == 0 ? V4 : MODE == 2 ? V4 / 2 : 0;   // float4 through DSMEM
+  constexpr int L2N = MODE == 3 ? 0 : V4 - DS;                 // float4 through L2
   if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
     if (DS) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar)), "r"(DS * 16) : "memory");
@@ -133,7 +134,7 @@ void run(float4* scratch, const float4* hin, float4* hout, size_t hbm_v4) {
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double bytes = (double)ncl * C * panels * BYTES;
   printf("C=%2d %-6s %-8s T=%d clusters=%d panels=%d: %.3f ms for %.0f MB exchanged (%.0f GB/s)\n", C,
-         MODE == 0 ? "DSMEM" : MODE == 1 ? "L2" : "mix", HBM ? "+hbm" : "", T, ncl, panels, ms, bytes / 1e6,
+         MODE == 0 ? "DSMEM" : MODE == 1 ? "L2" : MODE == 2 ? "mix" : "none", HBM ? "+hbm" : "", T, ncl, panels, ms, bytes / 1e6,
          bytes / ms / 1e6);
   CK(cudaFree(sink));
 }
@@ -157,6 +158,9 @@ int main() {
   run<16, 0, true, 256>(scratch, hin, hout, hbm_v4);
   run<16, 1, true, 256>(scratch, hin, hout, hbm_v4);
   run<16, 2, true, 256>(scratch, hin, hout, hbm_v4);
+  run<8, 3, true, 256>(scratch, hin, hout, hbm_v4);
+  run<16, 3, true, 256>(scratch, hin, hout, hbm_v4);
+  run<4, 3, true, 256>(scratch, hin, hout, hbm_v4);
   run<4, 0, true, 256>(scratch, hin, hout, hbm_v4);
   run<4, 1, true, 256>(scratch, hin, hout, hbm_v4);
   run<2, 1, true, 256>(scratch, hin, hout, hbm_v4);
