@@ -207,6 +207,20 @@ def measure_c4(args, peak, peak_kind):
     return out
 
 
+def launches(steps, rule, slab, cond, fallbacks, peer):
+    """libcssar kernel launches in the timed ita_iterate call (init + finalize = 2).  World 1:
+    S1..S5 + sel_coarse, fb_hist, fb_find, fb_collect, sel_fine (the fallback kernels exit early
+    when not needed) = 10 per iteration (k-rule), S1..S5 + the lambda step = 6 (fixed lambda).
+    Slab path: the sweeps + sel_coarse, three fine-level kernels and, when the iteration graph
+    gates the fallback round with a conditional node (cond), a set-condition kernel plus the
+    three fallback kernels only in the iterations that fell back; + 4 flag barriers with peer
+    transposes (the sparse-X' S1 adds its compact + fold kernels from iteration 1 on)."""
+    if not slab:
+        return steps * (10 if rule == "k" else 6) + 2
+    per = 5 + (4 + (1 if cond else 3) if rule == "k" else 1) + (4 if peer else 0) + (2 if peer and rule == "k" else 0)
+    return steps * per + (3 * fallbacks if cond and rule == "k" else 0) + 2
+
+
 def library_chain(Y, mask, k, mu, steps=10, warm=3):
     """SURVEY 8(d) "library chain" comparator (context, not the product and not a parity path):
     the same ITA iteration composed from torch.fft (cuFFT) and torch elementwise / topk ops in
@@ -398,6 +412,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     plan.status()                              # non-finite iterate -> CssarError
+    fallbacks_timed = plan.debug_fallbacks()
     ms = e0.elapsed_time(e1)
     clocks = sampler.stop()
     if world > 1:
@@ -447,8 +462,8 @@ def main():
                                "frac": iter_ach / (peak * world), "bytes_per_sample": ITER_BYTES_PER_SAMPLE,
                                "note": "aggregate over ranks; excludes NVLink transpose bytes" if world > 1 else None},
         "stages_ms": stages,
-        "gpu_launches": args.steps * ((10 if cfg.rule == "k" else 6) if not slab else
-                                       ((14 if world <= 8 else 12) if cfg.rule == "k" else 6)) + 2,
+        "gpu_launches": launches(args.steps, cfg.rule, slab, plan.debug_graph_info() if slab else 0,
+                                 fallbacks_timed, args.peer_transpose),
         "select_fallbacks": plan.debug_fallbacks(),
         "clocks": clocks,
     }
