@@ -972,7 +972,9 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
       if (*gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
       *ghave = false;
       // with the conditional fallback round first; if the capture or instantiation of that
-      // graph fails (e.g. collective work the conditional body cannot hold), once more without it
+      // graph fails (e.g. collective work the conditional body cannot hold), once more without it.
+      // On NCCL ranks the outcome is agreed collectively (every rank reaches the agreement), so
+      // all ranks replay graphs with the same collective sequence.
       for (int attempt = 0;; ++attempt) {
         cudaGraph_t g = nullptr;
         p0->cond_used = false;
@@ -982,14 +984,28 @@ int ita_multi(const Ranks& R, const void* const* Y, const uint32_t* const* mask,
         cudaError_t ei = cudaErrorUnknown;
         if (rc == CSSAR_OK && ec == cudaSuccess) ei = cudaGraphInstantiate(gexec, g, 0);
         if (g) cudaGraphDestroy(g);
-        if (rc == CSSAR_OK && ec == cudaSuccess && ei == cudaSuccess) break;
-        if (!p0->cond_used || attempt > 0) {
+        const bool ok = rc == CSSAR_OK && ec == cudaSuccess && ei == cudaSuccess;
+        bool all_ok = ok, same = true;
+        if (!R.group() && p0->transport == kTransportNccl) {
+          uint32_t w[2] = {ok ? 0u : 1u, p0->cond_used ? 1u : 0u};     // [failed ranks, ranks with the node]
+          if (cudaMemcpy(p0->d_bar, w, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+              nccl().allReduce(p0->d_bar, p0->d_bar, 2, ncclUint32, ncclSum, p0->comm, p0->cap_stream) != ncclSuccess ||
+              cudaStreamSynchronize(p0->cap_stream) != cudaSuccess ||
+              cudaMemcpy(w, p0->d_bar, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return CSSAR_ERR_NCCL;
+          all_ok = w[0] == 0u;
+          same = w[1] == 0u || w[1] == (uint32_t)p0->world;
+        }
+        if (all_ok && same) break;
+        if (ok && *gexec) { cudaGraphExecDestroy(*gexec); *gexec = nullptr; }
+        if (attempt > 0) {
           if (rc != CSSAR_OK) return rc;
           CUDA_TRY(ec);
           CUDA_TRY(ei);
+          return CSSAR_ERR_NCCL;                 // another rank could not capture the iteration
         }
         (void)cudaGetLastError();
-        p0->cond_ok = false;                   // retry with the unconditional fallback round
+        p0->cond_ok = false;                     // retry with the unconditional fallback round
       }
       *gkey = key;
       *ghave = true;
